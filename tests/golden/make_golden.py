@@ -1,0 +1,169 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (needs /root/reference, read-only):
+
+    python tests/golden/make_golden.py
+
+It imports the reference package under the alias ``qfswe_ref`` (it has no
+``__init__.py``) and writes small ``.npz`` fixtures next to this
+script.  The BASELINE manufactured solution is not admissible in the
+reference as shipped (scenario.py:72-77 rejects a non-zero mass residual),
+so the C1 case runs through the documented oracle extension: a subclass of
+the reference ``Discretization`` whose ``source_rhs`` adds the projected xi
+mass source, and a scenario built with ``manufacture=False`` whose momentum
+forcing follows the reference formula (scenario.py:78-93).
+"""
+
+from __future__ import annotations
+
+import importlib
+import sys
+import types
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REF = "/root/reference/pkg/src/qfswe"
+
+
+def load_reference():
+    if "qfswe_ref" not in sys.modules:
+        pkg = types.ModuleType("qfswe_ref")
+        pkg.__path__ = [REF]
+        sys.modules["qfswe_ref"] = pkg
+    return types.SimpleNamespace(**{
+        n: importlib.import_module(f"qfswe_ref.{n}")
+        for n in ("symbolic", "tensors", "mesh", "scenario", "solver", "harness")})
+
+
+def unit_square(R, n):
+    """BASELINE SW-NE split unit-square mesh, built as reference Mesh objects."""
+    xs = np.linspace(0.0, 1.0, n + 1)
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    verts = np.column_stack([X.ravel(), Y.ravel()])
+    tris = []
+    for i in range(n):
+        for j in range(n):
+            v00, v10 = i * (n + 1) + j, (i + 1) * (n + 1) + j
+            v11, v01 = (i + 1) * (n + 1) + j + 1, i * (n + 1) + j + 1
+            tris += [(v00, v10, v11), (v00, v11, v01)]
+    mesh = R.mesh.Mesh(vertices=verts, triangles=np.array(tris, dtype=np.int64))
+    R.mesh._build_edges(mesh)
+    return mesh
+
+
+def mms_scenario(R, **kw):
+    """BASELINE MMS as a reference Scenario (forcing per scenario.py:78-93)."""
+    import sympy as sp
+
+    S = R.scenario
+    X, Y, T = S.X, S.Y, S.T
+    xi = sp.sin(2 * sp.pi * (X + Y - T)) / 100
+    hb = 1 + X * Y / 10
+    H = hb + xi
+    U = H * sp.cos(2 * sp.pi * (X - T)) / 10
+    V = H * sp.sin(2 * sp.pi * (Y - T)) / 10
+    scn = S._build("mms", xi, U, V, hb, manufacture=False, **kw)
+    g = sp.Float(scn.g)
+    Fx = sp.diff(U, T) + sp.diff(U**2 / H, X) + sp.diff(U * V / H, Y) + g * H * sp.diff(xi, X)
+    Fy = sp.diff(V, T) + sp.diff(U * V / H, X) + sp.diff(V**2 / H, Y) + g * H * sp.diff(xi, Y)
+    scn.forcing = S._lambdify((X, Y, T), [Fx, Fy])
+    mass = S._lambdify((X, Y, T), [sp.diff(xi, T) + sp.diff(U, X) + sp.diff(V, Y)])
+    scn.mass_source = lambda x, y, t: mass(x, y, t)[0]
+    return scn
+
+
+def mms_discretization(R):
+    class MassSourceDiscretization(R.solver.Discretization):
+        """Oracle extension: xi mass source projected like solver.py:719-724."""
+
+        def source_rhs(self, state, t):
+            out = super().source_rhs(state, t)
+            x, y = self.quad_xy[:, :, 0], self.quad_xy[:, :, 1]
+            S = self.scn.mass_source(x, y, t)
+            out[:, 0] += self.geom.sqrt_detB[:, None] * ((S * self.quad_w) @ self.quad_phi.T)
+            return out
+    return MassSourceDiscretization
+
+
+def stage_terms(disc, state, t):
+    lam = disc.compute_lambda(state, t)
+    return dict(lam=lam, elem=disc.element_rhs(state), edge=disc.edge_rhs(state, t, lam),
+                src=disc.source_rhs(state, t))
+
+
+def perturbed_state(disc, state, seed):
+    rng = np.random.default_rng(seed)
+    c = state.c * (1.0 + 0.05 * rng.standard_normal(state.c.shape))
+    s = type(state)(c=c, u=np.zeros_like(state.u), t=state.t)
+    disc.solve_velocity(s)
+    return s
+
+
+def main():
+    R = load_reference()
+    # A. tensors
+    for k in range(4):
+        t = R.tensors.build_ref_tensors(k)
+        np.savez_compressed(HERE / f"tensors_k{k}.npz", **t.as_dict())
+    # B. reference-native perturbed square, k = 0..3
+    mesh = R.mesh.build_square_mesh(3, 0.2, 42)
+    for k in range(4):
+        scn = R.scenario.perturbed_square_scenario(dt=0.5)
+        disc = R.solver.Discretization(mesh, scn, k)
+        st0 = disc.project_initial()
+        sr = perturbed_state(disc, st0, 100 + k)
+        terms = stage_terms(disc, sr, 3.7)
+        st = st0
+        for _ in range(3):
+            st = disc.step(st)
+        np.savez_compressed(HERE / f"square_k{k}.npz", c0=st0.c, u0=st0.u, cr=sr.c, ur=sr.u,
+                            rhs_r=disc.rhs(sr, 3.7), c3=st.c, u3=st.u, **terms)
+    # C. lake at rest
+    mesh2 = R.mesh.build_square_mesh(2, 0.2, 5)
+    for k in (1, 2, 3):
+        scn = R.scenario.lake_at_rest_scenario(dt=0.5)
+        disc = R.solver.Discretization(mesh2, scn, k)
+        st0 = disc.project_initial()
+        st = st0
+        for _ in range(10):
+            st = disc.step(st)
+        np.savez_compressed(HERE / f"lake_k{k}.npz", c0=st0.c, rhs0=disc.rhs(st0, 0.0), c10=st.c)
+    # D. BASELINE C1 in full (MMS + mass source, p=1, N=32, RK2, 200 steps)
+    Disc = mms_discretization(R)
+    m32 = unit_square(R, 32)
+    scn = mms_scenario(R, dt=1e-4, t_end=0.02)
+    disc = Disc(m32, scn, 1)
+    st0 = disc.project_initial()
+    terms = stage_terms(disc, st0, 0.0)
+    st = disc.run(st0)
+    err = R.harness.l2_error(disc, st, st.t)
+    np.savez_compressed(HERE / "c1_mms_p1_n32.npz", c0=st0.c, u0=st0.u, c200=st.c, u200=st.u,
+                        t=st.t, err=np.array(err.errors()), **terms)
+    # E. small MMS p = 2, 3 (C2 shape at reduced size)
+    for k, n, steps in ((2, 8, 20), (3, 6, 10)):
+        m = unit_square(R, n)
+        scn = mms_scenario(R, dt=2e-5)
+        disc = Disc(m, scn, k)
+        st0 = disc.project_initial()
+        sr = perturbed_state(disc, st0, 7 + k)
+        terms = stage_terms(disc, sr, 0.3)
+        st = st0
+        for _ in range(steps):
+            st = disc.step(st)
+        np.savez_compressed(HERE / f"mms_p{k}_n{n}.npz", c0=st0.c, cr=sr.c, ur=sr.u,
+                            cN=st.c, uN=st.u, steps=steps, **terms)
+    # F. ring level 2, k = 1
+    mr = R.mesh.build_ring_mesh(2)
+    scn = R.scenario.ring_scenario(dt=0.5)
+    disc = R.solver.Discretization(mr, scn, 1)
+    st0 = disc.project_initial()
+    terms = stage_terms(disc, st0, 0.0)
+    st = disc.step(disc.step(st0))
+    np.savez_compressed(HERE / "ring_k1.npz", c0=st0.c, c2=st.c, **terms)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
