@@ -1,0 +1,138 @@
+/*
+ * qfswe.h — C ABI of the B200 (sm_100a) per-stage RHS path of the
+ * quadrature-free DG shallow-water solver (arXiv 1904.08684).
+ *
+ * Drop-in boundary for the reference Python package `qfswe`
+ * (/root/reference/pkg/src/qfswe/solver.py).  Every entry point replaces
+ * one reference method; the Python host mirror
+ * (paper_1904_08684_b200/solver.py) binds them with ctypes exactly as a
+ * maintainer of the reference would.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All `double*` / `int32_t*` arguments
+ *    are DEVICE pointers owned by the caller; the context only borrows them.
+ *  - State layout is structure-of-arrays, element index fastest:
+ *      c[3][K][ld] (xi, U, V),  u[2][K][ld] (u, v),  rhs like c,
+ *    K = (k+1)(k+2)/2, ld >= n_elem, ld % 32 == 0.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Every call returns a status: QF_OK, or QF_E_* below.  Asynchronous
+ *    numerical faults (dry state, singular projection, non-finite values)
+ *    are latched in a device error word read with qf_error().
+ *  - One context per (process, device); calls on one context must be
+ *    serialised by the caller (same as the reference's single-threaded
+ *    Discretization).
+ */
+#ifndef QFSWE_H
+#define QFSWE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QF_OK = 0,
+  QF_E_DRY = 1,        /* DryState          (solver.py:40-41, raised :308-311,:369-371,:403-404) */
+  QF_E_SINGULAR = 2,   /* SingularProjection (solver.py:44-45, raised :330-335) */
+  QF_E_NONFINITE = 3,  /* FloatingPointError (solver.py:768-769) */
+  QF_E_CUDA = 4,
+  QF_E_ARG = 5
+};
+
+/* error-word bits latched by the kernels */
+enum { QF_BIT_DRY = 1u, QF_BIT_SINGULAR = 2u, QF_BIT_NONFINITE = 4u };
+
+/* rhs term mask (reference rhs = element + edge + source, solver.py:727-741) */
+enum { QF_TERM_VOLUME = 1, QF_TERM_EDGE = 2, QF_TERM_SOURCE = 4, QF_TERM_ALL = 7 };
+
+/* device scenario families (paper_1904_08684_b200/scenario.py) */
+enum { QF_SCN_NONE = 0, QF_SCN_MMS = 1, QF_SCN_TRAVEL = 2, QF_SCN_LAKE = 3 };
+
+typedef struct qf_desc {
+  int32_t order;            /* k in 0..4 */
+  int32_t n_elem;           /* elements this context updates (owned) */
+  int64_t ld;               /* leading dimension of every [..][ld] table */
+  /* static element tables (device) */
+  const double* geo;        /* [6][ld]: B11, B12, B21, B22, a1x, a1y      (mesh.py:259-282) */
+  const double* hb;         /* [NH][ld]: P1 bathymetry, NH = 1 (k=0) or 3 (solver.py:139-168) */
+  const int32_t* nbr;       /* [3][ld]: neighbour codes (layout.py)        (mesh.py:79-107) */
+  int32_t n_bnd;            /* Dirichlet boundary slots */
+  const int32_t* bnd_elem;  /* [n_bnd] */
+  const int32_t* bnd_local; /* [n_bnd] */
+  double* ghost;            /* [n_bnd][5*(k+1)+6] scratch, written per stage */
+  /* physics (scenario.py:34-49) */
+  double g, f_c, tau_bf;
+  int32_t hb_linear;        /* hb_mode == "linear" */
+  int32_t scn_kind;         /* QF_SCN_* */
+  double scn_params[8];
+  int32_t has_forcing;      /* momentum forcing + xi mass source of the family */
+  int32_t block;            /* threads per block (0 = default) */
+} qf_desc;
+
+typedef struct qf_ctx qf_ctx;
+
+/* Discretization.__init__ (solver.py:103-124): bind tables, validate. */
+int qf_create(const qf_desc* desc, qf_ctx** out);
+void qf_destroy(qf_ctx* ctx);
+
+/* Discretization.solve_velocity (solver.py:315-336): u for elements
+ * [e0, e0+n) of state c (n < 0: all owned elements). */
+int qf_velocity(qf_ctx* ctx, const double* c, double* u, int32_t e0, int32_t n, void* stream);
+
+/* Dirichlet ghost traces at time t (solver.py:395-402, 636-653). */
+int qf_ghost(qf_ctx* ctx, double t, void* stream);
+
+/* Discretization.rhs / element_rhs / edge_rhs / source_rhs / compute_lambda
+ * (solver.py:340-741): rhs = sum of the masked terms at time t.
+ * lam (optional, [3][ld]): lambda of each element's local edges. */
+int qf_rhs(qf_ctx* ctx, const double* c, const double* u, double t, int32_t terms,
+           double* rhs, double* lam, void* stream);
+
+/* One SSP-RK stage (solver.py:750-764) for elements [e0, e0+n):
+ *   c_out = a*c0 + b*(c_in + dt*rhs(c_in, u_in, t)),  u_out = velocity(c_out).
+ * t_dev (optional device [2] = {t_step, dt}) overrides t: t = t_dev[0] + toff*t_dev[1]. */
+int qf_stage(qf_ctx* ctx, const double* c_in, const double* u_in, const double* c0,
+             double* c_out, double* u_out, double a, double b, double t, double dt,
+             const double* t_dev, double toff, int32_t e0, int32_t n, void* stream);
+
+/* Discretization.step (solver.py:745-770): one SSP-RK step in place on
+ * (c, u); `u` must hold velocity(c) on entry (qf_velocity).  `work` holds
+ * 2 * 5 * K * ld doubles.  t_dev: device [2] = {t, dt}; advanced by dt. */
+int qf_step(qf_ctx* ctx, double* c, double* u, double* work, double* t_dev, void* stream);
+
+/* Discretization.run (solver.py:772-780): n_steps steps, captured once in a
+ * CUDA graph (use_graph != 0) and replayed. */
+int qf_run(qf_ctx* ctx, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
+           int32_t use_graph, void* stream);
+
+/* State <-> device layout: aos [E][F][K] (reference State.c / State.u)
+ * <-> soa [F][K][ld]. */
+int qf_pack(const double* aos, double* soa, int32_t n_elem, int32_t F, int32_t K, int64_t ld,
+            void* stream);
+int qf_unpack(const double* soa, double* aos, int32_t n_elem, int32_t F, int32_t K, int64_t ld,
+              void* stream);
+
+/* gather / scatter rows for halo exchange: dst[r][i] = src[r][idx[i]] (rows
+ * of length ld / n_idx) and the inverse scatter. */
+int qf_gather(const double* src, int64_t ld_src, const int32_t* idx, int32_t n_idx,
+              int32_t rows, double* dst, void* stream);
+int qf_scatter(const double* src, const int32_t* idx, int32_t n_idx, int32_t rows,
+               double* dst, int64_t ld_dst, void* stream);
+
+/* Read (and optionally clear) the error word; synchronises `stream`. */
+int qf_error(qf_ctx* ctx, uint32_t* bits, int32_t clear, void* stream);
+
+/* Fill n doubles with v (L2 flush for timing). */
+int qf_fill(double* buf, size_t n, double v, void* stream);
+
+/* Number of kernel launches issued through this library (all contexts). */
+uint64_t qf_launch_count(void);
+const char* qf_last_error(void);
+int qf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QFSWE_H */

@@ -1,0 +1,766 @@
+// sm_100a kernels and the C ABI (include/qfswe.h) of the per-stage RHS path.
+//
+// Replaces, per SSP-RK stage, the reference's solve_velocity + rhs
+// (solver.py:315-741) and the RK combination (solver.py:756-764) with ONE
+// fused element kernel:
+//
+//   load c, u (own)  -> volume terms (factorised stiffness-triple contraction)
+//                    -> source terms (bathymetry gradient, friction, Coriolis,
+//                       manufactured forcing by on-device quadrature)
+//                    -> 3 edges: own + neighbour trace moments, lambda,
+//                       Lax-Friedrichs flux in 1-D trace space, lift
+//                       (owner-computes: no atomics, deterministic)
+//                    -> RK axpy with the stage base c0
+//                    -> velocity solve of the new state (LDL^T in registers)
+//   store c_out, u_out
+//
+// The velocity of the new state is solved in the epilogue, so the next
+// stage's neighbour gathers read (c, u) that are already consistent and the
+// reference's separate solve at the start of each stage disappears.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/qfswe.h"
+#include "qf_device.cuh"
+#include "generated/qf_order0.cuh"
+#include "generated/qf_order1.cuh"
+#include "generated/qf_order2.cuh"
+#include "generated/qf_order3.cuh"
+#include "generated/qf_order4.cuh"
+
+namespace qf {
+
+struct StageArgs {
+  const double* __restrict__ c;   // [3][K][ld]
+  const double* __restrict__ u;   // [2][K][ld]
+  const double* __restrict__ c0;  // RK base (may alias c_out)
+  double* c_out;                  // rhs out (mode 0) or new state (mode 1)
+  double* u_out;
+  double* lam;                    // [3][ld] optional
+  unsigned* err;
+  const double* t_dev;            // optional {t, dt}
+  double t, toff, dt, a, b;
+  int e0, n, terms, mode;
+};
+
+// ---------------------------------------------------------------- edges
+template <int k, int J>
+__device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
+                                          const double* c, const double* u, const double* hb,
+                                          double B11, double B12, double B21, double B22,
+                                          double sd, double isd, double* r) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NT = O::NT, NH = O::NH;
+  const int64_t ld = T.ld;
+  // own outward normal: physical image of the reference edge direction
+  constexpr double d1 = J == 0 ? -1.0 : (J == 1 ? 0.0 : 1.0);
+  constexpr double d2 = J == 0 ? 1.0 : (J == 1 ? -1.0 : 0.0);
+  const double dx = B11 * d1 + B12 * d2, dy = B21 * d1 + B22 * d2;
+  const double ln = sqrt(dx * dx + dy * dy);
+  const double n1 = dy / ln, n2 = -dx / ln;
+
+  double own[6][NT], oth[6][NT];
+#pragma unroll
+  for (int f = 0; f < 5; ++f) {
+    O::template trace<J>(f < 3 ? c + f * K : u + (f - 3) * K, own[f]);
+#pragma unroll
+    for (int a = 0; a < NT; ++a) own[f][a] *= isd;
+  }
+  O::template trace<J>(hb, own[5]);
+#pragma unroll
+  for (int a = 0; a < NT; ++a) own[5][a] *= isd;
+  double hbm_o = hb[0] * isd * 0.7071067811865476, hbm_n = hbm_o;
+
+  const int code = T.nbr[J * ld + e];
+  bool dirichlet = false;
+  const double* gp = nullptr;
+  if (code >= 0) {
+    const int nb = code >> 2, jn = code & 3;
+    const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
+    const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
+    const double nisd = 1.0 / sqrt(nB11 * nB22 - nB12 * nB21);
+    double f[K];
+#pragma unroll
+    for (int fi = 0; fi < 6; ++fi) {
+      if (fi < 5) {
+        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
+      } else {
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
+        hbm_n = f[0] * nisd * 0.7071067811865476;
+      }
+      O::trace_dyn(jn, f, oth[fi]);
+#pragma unroll
+      for (int a = 0; a < NT; ++a) oth[fi][a] *= (a & 1) ? -nisd : nisd;  // s -> 1-s
+    }
+  } else {
+    const int v = -1 - code, slot = v >> 1;
+    if ((v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
+      dirichlet = true;
+      gp = T.ghost + (int64_t)slot * (5 * NT + 6);
+#pragma unroll
+      for (int f = 0; f < 5; ++f)
+#pragma unroll
+        for (int a = 0; a < NT; ++a) oth[f][a] = ldg(gp + f * NT + a);
+    } else {  // reflective wall: mirror the normal components
+#pragma unroll
+      for (int a = 0; a < NT; ++a) {
+        const double qn = n1 * own[1][a] + n2 * own[2][a];
+        const double vn = n1 * own[3][a] + n2 * own[4][a];
+        oth[0][a] = own[0][a];
+        oth[1][a] = own[1][a] - 2.0 * n1 * qn;
+        oth[2][a] = own[2][a] - 2.0 * n2 * qn;
+        oth[3][a] = own[3][a] - 2.0 * n1 * vn;
+        oth[4][a] = own[4][a] - 2.0 * n2 * vn;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NT; ++a) oth[5][a] = own[5][a];
+  }
+
+  // lambda = max over both sides and s in {0, 1/2, 1} of |u.n| + sqrt(gH)
+  double unO[NT], unN[NT], tmp[NT], sH[3], sU[3];
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    unO[a] = n1 * own[3][a] + n2 * own[4][a];
+    unN[a] = n1 * oth[3][a] + n2 * oth[4][a];
+    tmp[a] = own[5][a] + own[0][a];
+  }
+  double lam = 0.0, hmin = 1.0;
+  O::samples(tmp, sH);
+  O::samples(unO, sU);
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    lam = fmax(lam, fabs(sU[s]) + sqrt(fmax(P.g * sH[s], 0.0)));
+    hmin = fmin(hmin, sH[s]);
+  }
+  if (dirichlet) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      sH[s] = ldg(gp + 5 * NT + s);
+      sU[s] = ldg(gp + 5 * NT + 3 + s);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < NT; ++a) tmp[a] = oth[5][a] + oth[0][a];
+    O::samples(tmp, sH);
+    O::samples(unN, sU);
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    lam = fmax(lam, fabs(sU[s]) + sqrt(fmax(P.g * sH[s], 0.0)));
+    hmin = fmin(hmin, sH[s]);
+  }
+  if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
+  if (A.lam) A.lam[J * ld + e] = lam;
+
+  // Lax-Friedrichs flux in trace space (reference solver.py:610-613)
+  double wO[NT], wN[NT], pO[NT], pN[NT], aO[NT], aN[NT], bO[NT], bN[NT];
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    wO[a] = 0.5 * own[0][a] + (P.hb_linear ? own[5][a] : 0.0);
+    wN[a] = 0.5 * oth[0][a] + (P.hb_linear ? oth[5][a] : 0.0);
+  }
+  O::jprod(own[0], wO, pO);
+  O::jprod(oth[0], wN, pN);
+  O::jprod(own[1], unO, aO);
+  O::jprod(oth[1], unN, aN);
+  O::jprod(own[2], unO, bO);
+  O::jprod(oth[2], unN, bN);
+  double Fx[NT], FU[NT], FV[NT];
+  const double hl = 0.5 * lam, g = P.g;
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    double pr = pO[a] + pN[a];
+    if (!P.hb_linear) pr += hbm_o * own[0][a] + hbm_n * oth[0][a];
+    Fx[a] = 0.5 * (n1 * (own[1][a] + oth[1][a]) + n2 * (own[2][a] + oth[2][a])) +
+            hl * (own[0][a] - oth[0][a]);
+    FU[a] = 0.5 * (aO[a] + aN[a] + g * n1 * pr) + hl * (own[1][a] - oth[1][a]);
+    FV[a] = 0.5 * (bO[a] + bN[a] + g * n2 * pr) + hl * (own[2][a] - oth[2][a]);
+  }
+  const double s = ln * isd;
+  O::template lift<J>(Fx, s, r);
+  O::template lift<J>(FU, s, r + K);
+  O::template lift<J>(FV, s, r + 2 * K);
+  (void)sd;
+}
+
+// ---------------------------------------------------------- stage kernel
+template <int k>
+__global__ void __launch_bounds__(128) stage_kernel(Tab T, Phys P, StageArgs A) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NH = O::NH;
+  const int e = A.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= A.e0 + A.n) return;
+  const int64_t ld = T.ld;
+  const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
+  const double dt = A.t_dev ? A.t_dev[1] : A.dt;
+  const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
+  const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
+  const double det = B11 * B22 - B12 * B21, sd = sqrt(det), isd = 1.0 / sd, idet = 1.0 / det;
+
+  double c[3 * K], u[2 * K], hb[K], r[3 * K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) c[i] = ldg(A.c + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) u[i] = ldg(A.u + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
+  const double* xi = c;
+  const double* cU = c + K;
+  const double* cV = c + 2 * K;
+
+  if (A.terms & TERM_VOL) {  // Eqs. (15)-(16), reference solver.py:410-485
+    double al[K], be[K], ra[K], rb[K], wv[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = B22 * cU[i] - B12 * cV[i];
+      be[i] = -B21 * cU[i] + B11 * cV[i];
+    }
+    O::vol_xi(al, be, ra);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[i] = ra[i] * idet;
+      al[i] = B22 * u[i] - B12 * u[K + i];   // a
+      be[i] = -B21 * u[i] + B11 * u[K + i];  // b
+      wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
+    }
+    const double g = P.g;
+    O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
+    const double i32 = idet * isd;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] = ra[i] * i32;
+      r[2 * K + i] = rb[i] * i32;
+    }
+    if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+      const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        al[i] = B22 * xi[i];
+        be[i] = -B21 * xi[i];
+      }
+      O::vol_xi(al, be, ra);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        al[i] = -B12 * xi[i];
+        be[i] = B11 * xi[i];
+      }
+      O::vol_xi(al, be, rb);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        r[K + i] += ghb * ra[i];
+        r[2 * K + i] += ghb * rb[i];
+      }
+    }
+  }
+  if (A.terms & TERM_SRC) {  // reference solver.py:708-725 (+ xi mass source)
+    double d1, d2;
+    O::hb_dref(hb, d1, d2);
+    const double i32 = idet * isd;
+    const double gx = P.g * (B22 * d1 - B21 * d2) * i32, gy = P.g * (-B12 * d1 + B11 * d2) * i32;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
+      r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
+    }
+    if (P.forcing) {
+      const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
+      double st, ct;
+      sincospi(2.0 * t, &st, &ct);
+      O::quad_project(
+          [&](double x1, double x2, double& f0, double& f1, double& f2) {
+            const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+            double S, Fx, Fy;
+            forcing(P, x, y, t, st, ct, S, Fx, Fy);
+            f0 = sd * S;
+            f1 = sd * Fx;
+            f2 = sd * Fy;
+          },
+          r, r + K, r + 2 * K);
+    }
+  }
+  if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
+    edge_term<k, 0>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
+    edge_term<k, 1>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
+    edge_term<k, 2>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
+  }
+  if (A.mode == 0) {
+#pragma unroll
+    for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = r[i];
+    return;
+  }
+  // SSP-RK combination (solver.py:756-764) and velocity of the new state
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) {
+    double v = c[i] + dt * r[i];
+    v = A.a != 0.0 ? fma(A.a, ldg(A.c0 + i * ld + e), A.b * v) : A.b * v;
+    c[i] = v;
+    fin = fin && isfinite(v);
+  }
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = c[i];
+  if (!fin) atomicOr(A.err, BIT_NONFINITE);
+  double uo[K], vo[K];
+  if (!solve_velocity<k>(c, c + K, c + 2 * K, hb, sd, uo, vo)) atomicOr(A.err, BIT_SINGULAR);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    A.u_out[i * ld + e] = uo[i];
+    A.u_out[(K + i) * ld + e] = vo[i];
+  }
+}
+
+template <int k>
+__global__ void __launch_bounds__(128)
+    velocity_kernel(Tab T, const double* __restrict__ c, double* __restrict__ u, int e0, int n,
+                    unsigned* err) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NH = O::NH;
+  const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e0 + n) return;
+  const int64_t ld = T.ld;
+  const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
+  const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
+  const double sd = sqrt(B11 * B22 - B12 * B21);
+  double cc[3 * K], hb[K], uo[K], vo[K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
+  if (!solve_velocity<k>(cc, cc + K, cc + 2 * K, hb, sd, uo, vo)) atomicOr(err, BIT_SINGULAR);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    u[i * ld + e] = uo[i];
+    u[(K + i) * ld + e] = vo[i];
+  }
+}
+
+// Dirichlet ghost table: Gauss moments of the exact (xi, U, V, u, v) on each
+// boundary edge plus (H, |u.n|) at the lambda samples (solver.py:395-402,
+// 636-653; the pinv projection of :649-653 reduces to these moments).
+template <int k>
+__global__ void ghost_kernel(Tab T, Phys P, const int* __restrict__ bel,
+                             const int* __restrict__ bloc, int nb, double tv,
+                             const double* t_dev, double toff, double* ghost) {
+  using O = Ord<k>;
+  constexpr int NT = O::NT;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nb) return;
+  const double t = t_dev ? t_dev[0] + toff * t_dev[1] : tv;
+  const int64_t ld = T.ld;
+  const int e = bel[s], j = bloc[s];
+  const double B11 = T.geo[e], B12 = T.geo[ld + e], B21 = T.geo[2 * ld + e], B22 = T.geo[3 * ld + e];
+  const double a1x = T.geo[4 * ld + e], a1y = T.geo[5 * ld + e];
+  // reference edge maps (x1, x2)(s): e0 (1-s, s), e1 (0, 1-s), e2 (s, 0)
+  const double x0 = j == 0 ? 1.0 : 0.0, xs = j == 0 ? -1.0 : (j == 2 ? 1.0 : 0.0);
+  const double y0 = j == 1 ? 1.0 : 0.0, ys = j == 0 ? 1.0 : (j == 1 ? -1.0 : 0.0);
+  const double dx = B11 * xs + B12 * ys, dy = B21 * xs + B22 * ys;
+  const double ln = sqrt(dx * dx + dy * dy), n1 = dy / ln, n2 = -dx / ln;
+  double mom[5 * NT];
+  O::gauss_moments(
+      [&](double sv, double* v) {
+        const double r1 = x0 + xs * sv, r2 = y0 + ys * sv;
+        const double x = a1x + B11 * r1 + B12 * r2, y = a1y + B21 * r1 + B22 * r2;
+        double xi, U, V;
+        exact3(P, x, y, t, xi, U, V);
+        const double H = hb_exact(P, x, y) + xi;
+        v[0] = xi;
+        v[1] = U;
+        v[2] = V;
+        v[3] = U / H;
+        v[4] = V / H;
+      },
+      mom);
+  double* out = ghost + (int64_t)s * (5 * NT + 6);
+#pragma unroll
+  for (int i = 0; i < 5 * NT; ++i) out[i] = mom[i];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double sv = 0.5 * q;
+    const double r1 = x0 + xs * sv, r2 = y0 + ys * sv;
+    const double x = a1x + B11 * r1 + B12 * r2, y = a1y + B21 * r1 + B22 * r2;
+    double xi, U, V;
+    exact3(P, x, y, t, xi, U, V);
+    const double H = hb_exact(P, x, y) + xi;
+    out[5 * NT + q] = H;
+    out[5 * NT + 3 + q] = fabs((U * n1 + V * n2) / H);
+  }
+}
+
+__global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
+
+__global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
+                            int K, int64_t ld) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  for (int i = 0; i < F * K; ++i) soa[i * ld + e] = aos[(int64_t)e * F * K + i];
+}
+
+__global__ void unpack_kernel(const double* __restrict__ soa, double* __restrict__ aos, int n,
+                              int F, int K, int64_t ld) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  for (int i = 0; i < F * K; ++i) aos[(int64_t)e * F * K + i] = soa[i * ld + e];
+}
+
+__global__ void gather_kernel(const double* __restrict__ src, int64_t ld, const int* __restrict__ idx,
+                              int n, int rows, double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = idx[i];
+  for (int r = 0; r < rows; ++r) dst[(int64_t)r * n + i] = src[r * ld + s];
+}
+
+__global__ void scatter_kernel(const double* __restrict__ src, const int* __restrict__ idx, int n,
+                               int rows, double* __restrict__ dst, int64_t ld) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int d = idx[i];
+  for (int r = 0; r < rows; ++r) dst[r * ld + d] = src[(int64_t)r * n + i];
+}
+
+__global__ void fill_kernel(double* buf, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = v;
+}
+
+}  // namespace qf
+
+// ===================================================================== ABI
+using namespace qf;
+
+struct qf_ctx {
+  qf_desc d;
+  Tab tab;
+  Phys phys;
+  unsigned* err;  // device error word
+  int K, NT, block;
+  // cached run graph
+  cudaGraphExec_t graph = nullptr;
+  const void* gkey[4] = {nullptr, nullptr, nullptr, nullptr};
+  int graph_launches = 0;
+};
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(QF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return QF_OK;
+}
+
+#define QF_DISPATCH(order, FN, ...)        \
+  switch (order) {                         \
+    case 0: FN<0>(__VA_ARGS__); break;     \
+    case 1: FN<1>(__VA_ARGS__); break;     \
+    case 2: FN<2>(__VA_ARGS__); break;     \
+    case 3: FN<3>(__VA_ARGS__); break;     \
+    default: FN<4>(__VA_ARGS__); break;    \
+  }
+
+template <int k>
+static void launch_stage(qf_ctx* x, const StageArgs& a, cudaStream_t s) {
+  const int bs = 128;
+  const int grid = (a.n + bs - 1) / bs;
+  if (grid == 0) return;
+  stage_kernel<k><<<grid, bs, 0, s>>>(x->tab, x->phys, a);
+  g_launches++;
+}
+
+template <int k>
+static void launch_velocity(qf_ctx* x, const double* c, double* u, int e0, int n, cudaStream_t s) {
+  const int bs = 128, grid = (n + bs - 1) / bs;
+  if (grid == 0) return;
+  velocity_kernel<k><<<grid, bs, 0, s>>>(x->tab, c, u, e0, n, x->err);
+  g_launches++;
+}
+
+template <int k>
+static void launch_ghost(qf_ctx* x, double t, const double* t_dev, double toff, cudaStream_t s) {
+  const int nb = x->d.n_bnd;
+  if (nb <= 0) return;
+  ghost_kernel<k><<<(nb + 127) / 128, 128, 0, s>>>(x->tab, x->phys, x->d.bnd_elem, x->d.bnd_local,
+                                                   nb, t, t_dev, toff, x->d.ghost);
+  g_launches++;
+}
+
+extern "C" {
+
+int qf_abi_version(void) { return 1; }
+const char* qf_last_error(void) { return g_last_error.c_str(); }
+uint64_t qf_launch_count(void) { return g_launches.load(); }
+
+int qf_create(const qf_desc* d, qf_ctx** out) {
+  if (!d || !out) return fail(QF_E_ARG, "null argument");
+  if (d->order < 0 || d->order > 4) return fail(QF_E_ARG, "order must be in 0..4");
+  if (d->n_elem < 0 || d->ld < d->n_elem || d->ld % 32) return fail(QF_E_ARG, "bad n_elem/ld");
+  if (!d->geo || !d->hb || !d->nbr) return fail(QF_E_ARG, "missing static tables");
+  if (d->n_bnd > 0 && (!d->bnd_elem || !d->bnd_local || !d->ghost))
+    return fail(QF_E_ARG, "missing Dirichlet boundary tables");
+  qf_ctx* x = new qf_ctx();
+  x->d = *d;
+  x->K = (d->order + 1) * (d->order + 2) / 2;
+  x->NT = d->order + 1;
+  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->ld};
+  x->phys.g = d->g;
+  x->phys.fc = d->f_c;
+  x->phys.tau = d->tau_bf;
+  x->phys.hb_linear = d->hb_linear;
+  x->phys.kind = d->scn_kind;
+  x->phys.forcing = d->has_forcing;
+  for (int i = 0; i < 8; ++i) x->phys.p[i] = d->scn_params[i];
+  if (cudaMalloc(&x->err, sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {
+    delete x;
+    return fail(QF_E_CUDA, "cudaMalloc(error word) failed");
+  }
+  *out = x;
+  return QF_OK;
+}
+
+void qf_destroy(qf_ctx* x) {
+  if (!x) return;
+  if (x->graph) cudaGraphExecDestroy(x->graph);
+  cudaFree(x->err);
+  delete x;
+}
+
+int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, void* stream) {
+  if (!x || !c || !u) return fail(QF_E_ARG, "null argument");
+  if (n < 0) {
+    e0 = 0;
+    n = x->d.n_elem;
+  }
+  QF_DISPATCH(x->d.order, launch_velocity, x, c, u, e0, n, (cudaStream_t)stream);
+  return cuda_check("velocity_kernel");
+}
+
+int qf_ghost(qf_ctx* x, double t, void* stream) {
+  if (!x) return fail(QF_E_ARG, "null ctx");
+  QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 0.0, (cudaStream_t)stream);
+  return cuda_check("ghost_kernel");
+}
+
+int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms, double* rhs,
+           double* lam, void* stream) {
+  if (!x || !c || !u || !rhs) return fail(QF_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (terms & TERM_EDGE) QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 0.0, s);
+  StageArgs a{};
+  a.c = c;
+  a.u = u;
+  a.c_out = rhs;
+  a.lam = lam;
+  a.err = x->err;
+  a.t = t;
+  a.e0 = 0;
+  a.n = x->d.n_elem;
+  a.terms = terms;
+  a.mode = 0;
+  QF_DISPATCH(x->d.order, launch_stage, x, a, s);
+  return cuda_check("stage_kernel(rhs)");
+}
+
+int qf_stage(qf_ctx* x, const double* c_in, const double* u_in, const double* c0, double* c_out,
+             double* u_out, double aa, double bb, double t, double dt, const double* t_dev,
+             double toff, int32_t e0, int32_t n, void* stream) {
+  if (!x || !c_in || !u_in || !c_out || !u_out) return fail(QF_E_ARG, "null argument");
+  if (aa != 0.0 && !c0) return fail(QF_E_ARG, "stage base c0 required");
+  if (n < 0) {
+    e0 = 0;
+    n = x->d.n_elem;
+  }
+  StageArgs a{};
+  a.c = c_in;
+  a.u = u_in;
+  a.c0 = c0;
+  a.c_out = c_out;
+  a.u_out = u_out;
+  a.err = x->err;
+  a.t_dev = t_dev;
+  a.t = t;
+  a.toff = toff;
+  a.dt = dt;
+  a.a = aa;
+  a.b = bb;
+  a.e0 = e0;
+  a.n = n;
+  a.terms = TERM_VOL | TERM_EDGE | TERM_SRC;
+  a.mode = 1;
+  QF_DISPATCH(x->d.order, launch_stage, x, a, (cudaStream_t)stream);
+  return cuda_check("stage_kernel");
+}
+
+}  // extern "C"
+
+// t_dev = {t, dt} lives on the device so one captured step is replayable.
+static void step_impl(qf_ctx* x, double* c, double* u, double* work, double* t_dev,
+                      cudaStream_t s) {
+  const int64_t S = (int64_t)5 * x->K * x->d.ld;  // one (c, u) state
+  const int64_t CU = (int64_t)3 * x->K * x->d.ld;
+  double* c1 = work;
+  double* u1 = work + CU;
+  double* c2 = work + S;
+  double* u2 = work + S + CU;
+  const int k = x->d.order;
+  auto stage = [&](const double* ci, const double* ui, const double* cb, double* co, double* uo,
+                   double a, double b, double toff) {
+    QF_DISPATCH(k, launch_ghost, x, 0.0, t_dev, toff, s);
+    StageArgs A{};
+    A.c = ci;
+    A.u = ui;
+    A.c0 = cb;
+    A.c_out = co;
+    A.u_out = uo;
+    A.err = x->err;
+    A.t_dev = t_dev;
+    A.toff = toff;
+    A.a = a;
+    A.b = b;
+    A.e0 = 0;
+    A.n = x->d.n_elem;
+    A.terms = TERM_VOL | TERM_EDGE | TERM_SRC;
+    A.mode = 1;
+    QF_DISPATCH(k, launch_stage, x, A, s);
+  };
+  // SSP-RK by order (solver.py:756-764); the last stage writes in place:
+  // each thread reads c0[e] before writing c_out[e] and no thread reads
+  // another element's c0 or the old u in that stage.
+  if (k == 0) {
+    stage(c, u, nullptr, c1, u1, 0.0, 1.0, 0.0);
+    cudaMemcpyAsync(c, c1, CU * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(u, u1, (S - CU) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  } else if (k == 1) {
+    stage(c, u, nullptr, c1, u1, 0.0, 1.0, 0.0);
+    stage(c1, u1, c, c, u, 0.5, 0.5, 1.0);
+  } else {
+    stage(c, u, nullptr, c1, u1, 0.0, 1.0, 0.0);
+    stage(c1, u1, c, c2, u2, 0.75, 0.25, 1.0);
+    stage(c2, u2, c, c, u, 1.0 / 3.0, 2.0 / 3.0, 0.5);
+  }
+  advance_time<<<1, 1, 0, s>>>(t_dev);
+  g_launches++;
+}
+
+extern "C" {
+
+int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* stream) {
+  if (!x || !c || !u || !work || !t_dev) return fail(QF_E_ARG, "null argument");
+  step_impl(x, c, u, work, t_dev, (cudaStream_t)stream);
+  return cuda_check("qf_step");
+}
+
+static int kernels_per_step(qf_ctx* x) {
+  const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
+  return stages * (1 + (x->d.n_bnd > 0 ? 1 : 0)) + 1;
+}
+
+int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
+           int32_t use_graph, void* stream) {
+  if (!x || !c || !u || !work || !t_dev) return fail(QF_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!use_graph || x->d.order == 0) {
+    for (int i = 0; i < n_steps; ++i) step_impl(x, c, u, work, t_dev, s);
+    return cuda_check("qf_run");
+  }
+  const void* key[4] = {c, u, work, t_dev};
+  if (!x->graph || memcmp(key, x->gkey, sizeof(key)) != 0) {
+    if (x->graph) {
+      cudaGraphExecDestroy(x->graph);
+      x->graph = nullptr;
+    }
+    cudaStream_t cap = s;
+    bool own = false;
+    if (s == nullptr) {
+      if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(QF_E_CUDA, "stream create failed");
+      own = true;
+    }
+    cudaGraph_t g;
+    if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return fail(QF_E_CUDA, "begin capture failed");
+    const uint64_t before = g_launches.load();
+    step_impl(x, c, u, work, t_dev, cap);
+    g_launches.store(before);
+    if (cudaStreamEndCapture(cap, &g) != cudaSuccess) return fail(QF_E_CUDA, "end capture failed");
+    cudaError_t e = cudaGraphInstantiate(&x->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (own) cudaStreamDestroy(cap);
+    if (e != cudaSuccess) return fail(QF_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    memcpy(x->gkey, key, sizeof(key));
+  }
+  for (int i = 0; i < n_steps; ++i) {
+    if (cudaGraphLaunch(x->graph, s) != cudaSuccess) return cuda_check("cudaGraphLaunch");
+  }
+  g_launches += (uint64_t)n_steps * kernels_per_step(x);
+  return cuda_check("qf_run");
+}
+
+int qf_error(qf_ctx* x, uint32_t* bits, int32_t clear, void* stream) {
+  if (!x || !bits) return fail(QF_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned h = 0;
+  if (cudaMemcpyAsync(&h, x->err, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return cuda_check("qf_error");
+  if (clear) cudaMemsetAsync(x->err, 0, sizeof(unsigned), s);
+  *bits = h;
+  return cuda_check("qf_error");
+}
+
+int qf_pack(const double* aos, double* soa, int32_t n, int32_t F, int32_t K, int64_t ld,
+            void* stream) {
+  if (n <= 0) return QF_OK;
+  pack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(aos, soa, n, F, K, ld);
+  g_launches++;
+  return cuda_check("pack_kernel");
+}
+
+int qf_unpack(const double* soa, double* aos, int32_t n, int32_t F, int32_t K, int64_t ld,
+              void* stream) {
+  if (n <= 0) return QF_OK;
+  unpack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(soa, aos, n, F, K, ld);
+  g_launches++;
+  return cuda_check("unpack_kernel");
+}
+
+int qf_gather(const double* src, int64_t ld, const int32_t* idx, int32_t n, int32_t rows,
+              double* dst, void* stream) {
+  if (n <= 0) return QF_OK;
+  gather_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(src, ld, idx, n, rows, dst);
+  g_launches++;
+  return cuda_check("gather_kernel");
+}
+
+int qf_scatter(const double* src, const int32_t* idx, int32_t n, int32_t rows, double* dst,
+               int64_t ld, void* stream) {
+  if (n <= 0) return QF_OK;
+  scatter_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(src, idx, n, rows, dst, ld);
+  g_launches++;
+  return cuda_check("scatter_kernel");
+}
+
+int qf_fill(double* buf, size_t n, double v, void* stream) {
+  fill_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(buf, n, v);
+  g_launches++;
+  return cuda_check("fill_kernel");
+}
+
+}  // extern "C"

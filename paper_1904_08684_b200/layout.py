@@ -1,0 +1,100 @@
+"""Device data layout: structure-of-arrays element tables (host-side build).
+
+Everything the stage kernels read is laid out field-major with the element
+index fastest, so a warp of 32 consecutive elements reads one 256-byte line
+per (field, mode):
+
+    state c   [3][K][ld]   (xi, U, V) modal coefficients
+    velocity  [2][K][ld]   (u, v)
+    geo       [6][ld]      B11, B12, B21, B22, a1x, a1y
+    hb        [NH][ld]     projected bathymetry coefficients (NH = 1 or 3)
+    nbr       [3][ld]      int32 neighbour code per local edge:
+                             >= 0 : 4 * neighbour + neighbour's local edge
+                             <  0 : boundary, -1 - (2 * slot + kind),
+                                    kind 0 = Dirichlet (slot indexes the
+                                    per-stage ghost table), 1 = wall
+    bnd       [nb]         (element, local edge) of each Dirichlet slot
+
+``ld`` = element count rounded up to a multiple of 32 (alignment of every
+row to 256 B).  Elements [E, ld) are padding and never touched; with a halo
+(multi-GPU partitions) owned elements come first and halo copies of
+neighbour-rank elements follow, see ``distributed.py``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .mesh import Mesh, compute_geometry
+
+__all__ = ["ElementTables", "build_tables", "pad_ld", "aos_to_soa", "soa_to_aos"]
+
+BND_DIRICHLET, BND_WALL = 0, 1
+
+
+def pad_ld(n: int) -> int:
+    return max(32, (n + 31) // 32 * 32)
+
+
+@dataclass
+class ElementTables:
+    n_elem: int
+    ld: int
+    geo: np.ndarray       # (6, ld) float64
+    nbr: np.ndarray       # (3, ld) int32
+    bnd_elem: np.ndarray  # (nb,) int32
+    bnd_local: np.ndarray  # (nb,) int32
+    detB: np.ndarray      # (E,)
+    h_min: float
+
+
+def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, n_alloc: int | None = None
+                 ) -> ElementTables:
+    """Geometry and neighbour codes for ``mesh`` (all elements owned)."""
+    geom, egeom = compute_geometry(mesh)
+    E = mesh.n_triangles
+    ld = pad_ld(n_alloc or E)
+    geo = np.zeros((6, ld))
+    geo[0, :E], geo[1, :E] = geom.B[:, 0, 0], geom.B[:, 0, 1]
+    geo[2, :E], geo[3, :E] = geom.B[:, 1, 0], geom.B[:, 1, 1]
+    geo[4, :E], geo[5, :E] = geom.a1[:, 0], geom.a1[:, 1]
+    c = mesh.conn
+    code = np.zeros((3, ld), dtype=np.int64)
+    inner = c.nbr >= 0
+    code[:, :E] = np.where(inner, 4 * c.nbr + np.maximum(c.nbr_local, 0), 0).T
+    bel, bj = np.nonzero(~inner)
+    marks = -c.nbr_local[bel, bj]
+    dmask = np.isin(marks, list(dirichlet_markers))
+    wmask = np.isin(marks, list(wall_markers))
+    if not (dmask | wmask).all():
+        bad = int(np.flatnonzero(~(dmask | wmask))[0])
+        raise ValueError(f"boundary edge of element {bel[bad]} has marker {marks[bad]}; "
+                         "only Dirichlet and wall markers are supported")
+    # Dirichlet slots in mesh-edge order (reference pass_B order, solver.py:213-216)
+    eidx = c.elem_edge[bel, bj]
+    order = np.argsort(eidx, kind="stable")
+    bel, bj, dmask = bel[order], bj[order], dmask[order]
+    slot = np.cumsum(dmask) - 1
+    code[bj, bel] = np.where(dmask, -1 - (2 * slot + BND_DIRICHLET), -1 - (2 * 0 + BND_WALL))
+    if E and code.max() >= 2**31:
+        raise ValueError("mesh too large for int32 neighbour codes")
+    # CFL height (solver.py:240-246)
+    lens = egeom.length[c.elem_edge]
+    h_min = float((geom.detB / lens.max(axis=1)).min()) if E else 0.0
+    return ElementTables(n_elem=E, ld=ld, geo=geo, nbr=code.astype(np.int32),
+                         bnd_elem=bel[dmask].astype(np.int32),
+                         bnd_local=bj[dmask].astype(np.int32), detB=geom.detB, h_min=h_min)
+
+
+def aos_to_soa(a: np.ndarray, ld: int) -> np.ndarray:
+    """(E, F, K) -> (F, K, ld) with zero padding."""
+    E, F, K = a.shape
+    out = np.zeros((F, K, ld))
+    out[:, :, :E] = a.transpose(1, 2, 0)
+    return out
+
+
+def soa_to_aos(s: np.ndarray, E: int) -> np.ndarray:
+    return np.ascontiguousarray(s[:, :, :E].transpose(2, 0, 1))

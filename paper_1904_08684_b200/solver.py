@@ -1,0 +1,440 @@
+"""Discretization / State: the reference's solver API on the B200 path.
+
+Drop-in for reference ``qfswe.solver`` (solver.py:28-34, 48-780):
+``State(c, u, t)``, ``Discretization(mesh, scenario, order, backend)`` with
+``project_volume``, ``project_initial``, ``solve_velocity``,
+``compute_lambda``, ``element_rhs``, ``edge_rhs``, ``source_rhs``, ``rhs``,
+``step``, ``run`` and the same exceptions (``DryState``,
+``SingularProjection``, ``FloatingPointError``, ``ValueError``, CFL
+``UserWarning``).
+
+All per-stage work runs in the sm_100a kernels behind the C ABI
+(``_cabi.py`` -> ``libqfswe.so``); the state stays device-resident in a
+structure-of-arrays layout between steps and ``State.c`` / ``State.u`` are
+materialised lazily.  Setup (geometry, quadrature, bathymetry projection)
+stays on the host, vectorised in NumPy.  There is no CPU fallback: without
+the library or a CUDA device the constructor raises.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+
+from . import _cabi
+from .layout import BND_DIRICHLET, build_tables, pad_ld
+from .mesh import Mesh, compute_geometry
+from .scenario import KIND_NONE, Scenario
+from .symbolic import build_basis
+from .tensors import build_ref_tensors, triangle_rule
+
+__all__ = ["DryState", "SingularProjection", "State", "Discretization", "flux_dot_n"]
+
+XI, U, V = 0, 1, 2
+
+
+class DryState(ArithmeticError):
+    """Total water depth at or below the configured minimum."""
+
+
+class SingularProjection(ArithmeticError):
+    """Per-element velocity projection system is numerically singular."""
+
+
+def flux_dot_n(xi, Uq, Vq, uu, uv, hb, n1, n2, g):
+    """Pointwise modified flux . n (reference solver.py:60-71), test oracle."""
+    pressure = 0.5 * g * xi * (xi + 2.0 * hb)
+    return (Uq * n1 + Vq * n2, (Uq * uu + pressure) * n1 + (Uq * uv) * n2,
+            (Vq * uu) * n1 + (Vq * uv + pressure) * n2)
+
+
+class State:
+    """Modal coefficients c[e, j, i] (xi, U, V) and u[e, j, i] (u, v) at time t.
+
+    Host arrays are materialised lazily from the device copy; once they are
+    handed out the device copy is dropped (the caller may mutate them), so a
+    later ``step`` re-uploads.
+    """
+
+    def __init__(self, c=None, u=None, t: float = 0.0, _dev=None):
+        self._c = c
+        self._u = u
+        self.t = float(t)
+        self._dev = _dev  # (disc, DeviceState)
+
+    def _materialise(self):
+        if self._dev is not None and (self._c is None or self._u is None):
+            disc, ds = self._dev
+            self._c, self._u = disc._download(ds)
+            self._dev = None
+
+    @property
+    def c(self) -> np.ndarray:
+        self._materialise()
+        return self._c
+
+    @c.setter
+    def c(self, v):
+        self._materialise()
+        self._c = v
+
+    @property
+    def u(self) -> np.ndarray:
+        self._materialise()
+        return self._u
+
+    @u.setter
+    def u(self, v):
+        self._materialise()
+        self._u = v
+
+    def copy(self) -> "State":
+        if self._dev is not None and self._c is None:
+            disc, ds = self._dev
+            return State(t=self.t, _dev=(disc, ds.clone()))
+        return State(self.c.copy(), self.u.copy(), self.t)
+
+
+class DeviceState:
+    """(c, u) in SoA layout on the device plus the device time {t, dt}."""
+
+    def __init__(self, c, u, t_dev):
+        self.c, self.u, self.t_dev = c, u, t_dev
+
+    def clone(self) -> "DeviceState":
+        return DeviceState(self.c.clone(), self.u.clone(), self.t_dev.clone())
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 path needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+class Discretization:
+    """Mesh + order + scenario bound to device tables (reference solver.py:100-124)."""
+
+    def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
+                 device: int | None = None):
+        if backend not in ("einsum", "ir"):
+            raise ValueError("backend must be 'einsum' or 'ir'")
+        if scenario.hb_mode not in ("linear", "const"):
+            raise ValueError("hb_mode must be 'linear' or 'const'")
+        self.mesh = mesh
+        self.scn = scenario
+        self.k = int(order)
+        self.backend = backend  # accepted for signature compatibility only
+        self.basis = build_basis(self.k)
+        self.K = self.basis.size
+        self.geom, self.edge_geom = compute_geometry(mesh)
+        self._setup_quadrature()
+        self._setup_bathymetry()
+        self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers)
+        self.h_min = self.tables.h_min
+        needs_data = len(self.tables.bnd_elem) > 0 or scenario.forcing is not None \
+            or scenario.mass_source is not None
+        if needs_data and scenario.device.kind == KIND_NONE:
+            raise ValueError(f"scenario {scenario.name!r} needs boundary data or forcing that "
+                             "has no device evaluator (use a closed-form scenario family)")
+        self._cfl_warned = False
+        self.cfl_warn_threshold = 2.0
+        self.dt = scenario.dt
+        self._dt_fixed = scenario.cfl is None
+        self.phi_at_vertices = np.array(
+            [[f.eval(*v) for v in ((0.0, 0.0), (1.0, 0.0), (0.0, 1.0))]
+             for f in self.basis.functions])
+        self._setup_device(device)
+
+    # ------------------------------------------------------------- setup
+    @property
+    def tensors(self):
+        """Reference-form tensors (exact; lazily built, not used by the kernels)."""
+        return build_ref_tensors(self.k)
+
+    def _setup_quadrature(self):
+        pts, wts = triangle_rule(2 * self.k + 2)
+        self.quad_ref, self.quad_w = pts, wts
+        self.quad_phi = np.array([f.eval(pts[:, 0], pts[:, 1]) for f in self.basis.functions])
+        B, a1 = self.geom.B, self.geom.a1
+        self.quad_xy = np.einsum("eab,qb->eqa", B, pts) + a1[:, None, :]
+
+    def _setup_bathymetry(self):
+        """P1 projection of h_b and its constant gradient (solver.py:139-168)."""
+        sd = self.geom.sqrt_detB
+        vals = self.scn.hb(self.quad_xy[:, :, 0], self.quad_xy[:, :, 1])
+        keep = 1 if self.k == 0 else 3
+        proj = sd[:, None] * ((vals * self.quad_w) @ self.quad_phi[:keep].T)
+        self.hb_coef = np.zeros((len(sd), self.K))
+        self.hb_coef[:, :keep] = proj
+        if keep == 3:
+            g1 = np.array([float(self.basis.gradients[i][0].eval(0.0, 0.0)) for i in range(3)])
+            g2 = np.array([float(self.basis.gradients[i][1].eval(0.0, 0.0)) for i in range(3)])
+            d1, d2 = proj @ g1, proj @ g2
+            B, det = self.geom.B, self.geom.detB
+            sc = det * sd
+            self.hb_grad = np.column_stack([(B[:, 1, 1] * d1 - B[:, 1, 0] * d2) / sc,
+                                            (-B[:, 0, 1] * d1 + B[:, 0, 0] * d2) / sc])
+        else:
+            self.hb_grad = np.zeros((len(sd), 2))
+        self.hb_mean = self.hb_coef[:, 0] / (math.sqrt(2.0) * sd)
+        self._nh = keep
+
+    def _setup_device(self, device):
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        lib = _cabi.load()
+        tb = self.tables
+        E, ld = tb.n_elem, tb.ld
+        self.ld = ld
+        dev = self.device
+        self._geo = torch.from_numpy(tb.geo).to(dev)
+        hb = np.zeros((self._nh, ld))
+        hb[:, :E] = self.hb_coef[:, : self._nh].T
+        self._hb = torch.from_numpy(hb).to(dev)
+        self._nbr = torch.from_numpy(tb.nbr).to(dev)
+        nb = len(tb.bnd_elem)
+        self._bel = torch.from_numpy(tb.bnd_elem).to(dev)
+        self._bloc = torch.from_numpy(tb.bnd_local).to(dev)
+        self._ghost = torch.zeros(max(nb, 1) * (5 * (self.k + 1) + 6), dtype=torch.float64,
+                                  device=dev)
+        scn = self.scn
+        d = _cabi.QfDesc()
+        d.order, d.n_elem, d.ld = self.k, E, ld
+        d.geo, d.hb, d.nbr = self._geo.data_ptr(), self._hb.data_ptr(), self._nbr.data_ptr()
+        d.n_bnd = nb
+        d.bnd_elem, d.bnd_local = self._bel.data_ptr(), self._bloc.data_ptr()
+        d.ghost = self._ghost.data_ptr()
+        d.g, d.f_c, d.tau_bf = scn.g, scn.f_c, scn.tau_bf
+        d.hb_linear = 1 if scn.hb_mode == "linear" else 0
+        d.scn_kind = scn.device.kind
+        for i, p in enumerate(scn.device.as_array()):
+            d.scn_params[i] = float(p)
+        d.has_forcing = 1 if (scn.forcing is not None or scn.mass_source is not None) else 0
+        self._desc = d
+        ctx = _cabi.C.c_void_p()
+        _cabi.check(lib.qf_create(_cabi.C.byref(d), _cabi.C.byref(ctx)), "qf_create")
+        self._ctx = ctx
+        self._lib = lib
+        self._work = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_ctx", None):
+                self._lib.qf_destroy(self._ctx)
+                self._ctx = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------- device state
+    @property
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def _empty_state(self):
+        t = self.torch
+        return (t.empty((3, self.K, self.ld), dtype=t.float64, device=self.device),
+                t.empty((2, self.K, self.ld), dtype=t.float64, device=self.device))
+
+    def _upload_c(self, c_host: np.ndarray):
+        t = self.torch
+        E = self.tables.n_elem
+        a = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64))
+        if self.device.type == "cuda":
+            a = a.pin_memory()
+        a = a.to(self.device, non_blocking=True)
+        c, _ = self._empty_state()
+        c.zero_()
+        _cabi.check(self._lib.qf_pack(a.data_ptr(), c.data_ptr(), E, 3, self.K, self.ld,
+                                      self._stream), "qf_pack")
+        return c
+
+    def _download(self, ds: DeviceState):
+        t = self.torch
+        E = self.tables.n_elem
+        ca = t.empty((E, 3, self.K), dtype=t.float64, device=self.device)
+        ua = t.empty((E, 2, self.K), dtype=t.float64, device=self.device)
+        s = self._stream
+        _cabi.check(self._lib.qf_unpack(ds.c.data_ptr(), ca.data_ptr(), E, 3, self.K, self.ld, s),
+                    "qf_unpack")
+        _cabi.check(self._lib.qf_unpack(ds.u.data_ptr(), ua.data_ptr(), E, 2, self.K, self.ld, s),
+                    "qf_unpack")
+        return ca.cpu().numpy(), ua.cpu().numpy()
+
+    def _soa_to_host(self, x, F):
+        t = self.torch
+        E = self.tables.n_elem
+        a = t.empty((E, F, self.K), dtype=t.float64, device=self.device)
+        _cabi.check(self._lib.qf_unpack(x.data_ptr(), a.data_ptr(), E, F, self.K, self.ld,
+                                        self._stream), "qf_unpack")
+        return a.cpu().numpy()
+
+    def to_device(self, state: State, solve: bool = True) -> DeviceState:
+        """Device copy of ``state`` (re-used when the state came from the device)."""
+        if state._dev is not None and state._c is None and state._dev[0] is self:
+            return state._dev[1]
+        c = self._upload_c(state.c)
+        _, u = self._empty_state()
+        u.zero_()
+        if solve:
+            self._check(self._lib.qf_velocity(self._ctx, c.data_ptr(), u.data_ptr(), 0, -1,
+                                              self._stream), "qf_velocity")
+        tdev = self.torch.tensor([state.t, self.dt], dtype=self.torch.float64, device=self.device)
+        return DeviceState(c, u, tdev)
+
+    def _check(self, status, what):
+        _cabi.check(status, what)
+
+    def _raise_errors(self, where: str):
+        bits = _cabi.C.c_uint32(0)
+        _cabi.check(self._lib.qf_error(self._ctx, _cabi.C.byref(bits), 1, self._stream),
+                    "qf_error")
+        b = bits.value
+        if b & _cabi.BIT_DRY:
+            raise DryState(f"non-positive depth at an edge sample ({where})")
+        if b & _cabi.BIT_SINGULAR:
+            raise SingularProjection(f"velocity projection is singular ({where})")
+        if b & _cabi.BIT_NONFINITE:
+            raise FloatingPointError(f"non-finite state ({where})")
+
+    # ------------------------------------------------- projection helpers
+    def project_volume(self, fn, t: float | None = None) -> np.ndarray:
+        x, y = self.quad_xy[:, :, 0], self.quad_xy[:, :, 1]
+        vals = fn(x, y) if t is None else fn(x, y, t)
+        return self.geom.sqrt_detB[:, None] * ((vals * self.quad_w) @ self.quad_phi.T)
+
+    def project_initial(self) -> State:
+        """Project analytic (or non-analytic ``initial``) data at t = 0 (solver.py:288-303)."""
+        scn = self.scn
+        x, y = self.quad_xy[:, :, 0], self.quad_xy[:, :, 1]
+        if scn.initial is not None:
+            fields = scn.initial(x, y)
+        elif scn.exact is not None:
+            fields = scn.exact(x, y, 0.0)
+        else:
+            raise ValueError("scenario has no analytic solution to project")
+        sd = self.geom.sqrt_detB[:, None]
+        c = np.stack([sd * ((f * self.quad_w) @ self.quad_phi.T) for f in fields], axis=1)
+        H = (self.hb_coef + c[:, XI]) @ self.quad_phi / self.geom.sqrt_detB[:, None]
+        if (H < scn.h_min).any():
+            raise DryState(f"projected depth fell below h_min = {scn.h_min}")
+        state = State(c=c, u=np.zeros((len(c), 2, self.K)), t=0.0)
+        self.solve_velocity(state)
+        if not self._dt_fixed:
+            self.dt = self.cfl_dt(state)
+            self._dt_fixed = True
+        return state
+
+    def cfl_dt(self, state: State) -> float:
+        """dt = cfl * h_min / max lambda(t) (extension)."""
+        lam = self.compute_lambda(state, state.t)
+        return float(self.scn.cfl) * self.h_min / float(lam.max())
+
+    # --------------------------------------------------------- operators
+    def solve_velocity(self, state: State) -> None:
+        """Per-element H-weighted projection solve, in place on state.u (solver.py:315-336)."""
+        c = self._upload_c(state.c)
+        _, u = self._empty_state()
+        self._check(self._lib.qf_velocity(self._ctx, c.data_ptr(), u.data_ptr(), 0, -1,
+                                          self._stream), "qf_velocity")
+        self._raise_errors("solve_velocity")
+        state.u[:] = self._soa_to_host(u, 2)
+
+    def _rhs_terms(self, state: State, t: float, terms: int, want_lam=False):
+        c = self._upload_c(state.c)
+        _, u = self._empty_state()
+        u.zero_()
+        uh = np.ascontiguousarray(state.u, dtype=np.float64)
+        ua = self.torch.from_numpy(uh).to(self.device)
+        self._check(self._lib.qf_pack(ua.data_ptr(), u.data_ptr(), self.tables.n_elem, 2, self.K,
+                                      self.ld, self._stream), "qf_pack")
+        out, _ = self._empty_state()
+        lam = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device) \
+            if want_lam else None
+        self._check(self._lib.qf_rhs(self._ctx, c.data_ptr(), u.data_ptr(), float(t), terms,
+                                     out.data_ptr(), lam.data_ptr() if want_lam else None,
+                                     self._stream), "qf_rhs")
+        self._raise_errors("rhs")
+        r = self._soa_to_host(out, 3)
+        if want_lam:
+            return r, lam[:, : self.tables.n_elem].cpu().numpy()
+        return r
+
+    def compute_lambda(self, state: State, t: float) -> np.ndarray:
+        """Per-edge LF speed in ``mesh.edges`` order (solver.py:340-406)."""
+        _, lam = self._rhs_terms(state, t, _cabi.TERM_EDGE, want_lam=True)
+        c = self.mesh.conn
+        return lam[c.left_local, c.left]
+
+    def element_rhs(self, state: State) -> np.ndarray:
+        return self._rhs_terms(state, 0.0, _cabi.TERM_VOLUME)
+
+    def edge_rhs(self, state: State, t: float, lam: np.ndarray | None = None) -> np.ndarray:
+        """Edge terms; ``lam`` is accepted for signature compatibility (the
+        kernel recomputes the identical per-edge lambda on the device)."""
+        return self._rhs_terms(state, t, _cabi.TERM_EDGE)
+
+    def source_rhs(self, state: State, t: float) -> np.ndarray:
+        return self._rhs_terms(state, t, _cabi.TERM_SOURCE)
+
+    def rhs(self, state: State, t: float) -> np.ndarray:
+        r, lam = self._rhs_terms(state, t, _cabi.TERM_ALL, want_lam=True)
+        self._cfl_advisory(float(lam.max()))
+        return r
+
+    def _cfl_advisory(self, lam_max: float):
+        if not self._cfl_warned:
+            cfl = self.dt * lam_max / self.h_min
+            if cfl > self.cfl_warn_threshold:
+                warnings.warn(f"CFL advisory: dt*lambda_max/h_min = {cfl:.2f} exceeds "
+                              f"{self.cfl_warn_threshold}", stacklevel=3)
+            self._cfl_warned = True
+
+    # ------------------------------------------------------ time stepping
+    def _work_buf(self):
+        if self._work is None:
+            self._work = self.torch.empty(2 * 5 * self.K * self.ld, dtype=self.torch.float64,
+                                          device=self.device)
+        return self._work
+
+    def step_device(self, ds: DeviceState, n_steps: int = 1, use_graph: bool = True) -> None:
+        """Advance a device state in place by n_steps (no host traffic)."""
+        w = self._work_buf()
+        if n_steps == 1:
+            st = self._lib.qf_step(self._ctx, ds.c.data_ptr(), ds.u.data_ptr(), w.data_ptr(),
+                                   ds.t_dev.data_ptr(), self._stream)
+            self._check(st, "qf_step")
+        elif n_steps > 1:
+            st = self._lib.qf_run(self._ctx, n_steps, ds.c.data_ptr(), ds.u.data_ptr(),
+                                  w.data_ptr(), ds.t_dev.data_ptr(), 1 if use_graph else 0,
+                                  self._stream)
+            self._check(st, "qf_run")
+
+    def step(self, state: State) -> State:
+        """One SSP-RK step; returns a new State, input unchanged (solver.py:745-770)."""
+        ds = self.to_device(state).clone() if state._dev is not None else self.to_device(state)
+        ds.t_dev[1] = self.dt
+        if not self._cfl_warned:
+            self._cfl_advisory(float(self.compute_lambda(State(t=state.t, _dev=(self, ds.clone())),
+                                                         state.t).max()))
+        self.step_device(ds, 1)
+        self._raise_errors(f"step to t = {state.t + self.dt}")
+        return State(t=state.t + self.dt, _dev=(self, ds))
+
+    def run(self, state: State | None = None, t_end: float | None = None) -> State:
+        if state is None:
+            state = self.project_initial()
+        t_end = self.scn.t_end if t_end is None else t_end
+        n_steps = int(round((t_end - state.t) / self.dt))
+        ds = self.to_device(state)
+        if state._dev is not None:
+            ds = ds.clone()
+        ds.t_dev[1] = self.dt
+        self.step_device(ds, n_steps)
+        self._raise_errors(f"run to t = {t_end}")
+        t = float(ds.t_dev[0].item())
+        return State(t=t, _dev=(self, ds))

@@ -1,0 +1,128 @@
+"""GPU parity: sm_100a kernels (through the C ABI) vs the reference fixtures
+and the CPU oracle.  Tolerance: 1e-11 relative L2 per field (north star)."""
+
+import numpy as np
+import pytest
+
+from conftest import field_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+def _disc(mesh, scn, k):
+    from paper_1904_08684_b200.solver import Discretization
+    return Discretization(mesh, scn, k)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_square_terms_vs_reference(golden, k):
+    """Reference-native perturbed square (build_square_mesh(3, 0.2, 42))."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import State
+    g = golden(f"square_k{k}.npz")
+    disc = _disc(M.build_square_mesh(3, 0.2, 42), S.perturbed_square_scenario(dt=0.5), k)
+    st0 = disc.project_initial()
+    assert field_rel(st0.c, g["c0"]) < TOL
+    assert field_rel(st0.u, g["u0"]) < TOL
+    sr = State(g["cr"].copy(), np.zeros_like(g["ur"]), 0.0)
+    disc.solve_velocity(sr)
+    assert field_rel(sr.u, g["ur"]) < TOL
+    sr = State(g["cr"].copy(), g["ur"].copy(), 0.0)
+    assert rel_l2(disc.compute_lambda(sr, 3.7), g["lam"]) < TOL
+    assert field_rel(disc.element_rhs(sr), g["elem"]) < TOL
+    assert field_rel(disc.edge_rhs(sr, 3.7), g["edge"]) < TOL
+    assert field_rel(disc.source_rhs(sr, 3.7), g["src"]) < TOL
+    assert field_rel(disc.rhs(sr, 3.7), g["rhs_r"]) < TOL
+    st = st0
+    for _ in range(3):
+        st = disc.step(st)
+    assert field_rel(st.c, g["c3"]) < TOL
+    assert field_rel(st.u, g["u3"]) < TOL
+
+
+def test_c1_full_run_vs_reference(golden):
+    """BASELINE C1 in full: p=1, N=32, SSP-RK2, dt=1e-4, 200 steps."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    g = golden("c1_mms_p1_n32.npz")
+    disc = _disc(M.build_unit_square_mesh(32), S.mms_scenario(dt=1e-4, t_end=0.02), 1)
+    st0 = disc.project_initial()
+    assert field_rel(st0.c, g["c0"]) < TOL
+    assert rel_l2(disc.compute_lambda(st0, 0.0), g["lam"]) < TOL
+    assert field_rel(disc.edge_rhs(st0, 0.0), g["edge"]) < TOL
+    assert field_rel(disc.source_rhs(st0, 0.0), g["src"]) < TOL
+    out = disc.run(st0)
+    assert abs(out.t - 0.02) < 1e-12
+    assert field_rel(out.c, g["c200"]) < TOL
+    assert field_rel(out.u, g["u200"]) < TOL
+
+
+@pytest.mark.parametrize("k,n", [(2, 8), (3, 6)])
+def test_mms_small_vs_reference(golden, k, n):
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import State
+    g = golden(f"mms_p{k}_n{n}.npz")
+    disc = _disc(M.build_unit_square_mesh(n), S.mms_scenario(dt=2e-5), k)
+    st0 = disc.project_initial()
+    sr = State(g["cr"].copy(), g["ur"].copy(), 0.0)
+    assert field_rel(disc.edge_rhs(sr, 0.3), g["edge"]) < TOL
+    assert field_rel(disc.source_rhs(sr, 0.3), g["src"]) < TOL
+    assert field_rel(disc.element_rhs(sr), g["elem"]) < TOL
+    out = disc.run(st0, t_end=int(g["steps"]) * 2e-5)
+    assert field_rel(out.c, g["cN"]) < TOL
+
+
+def test_ring_vs_reference(golden):
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    g = golden("ring_k1.npz")
+    disc = _disc(M.build_ring_mesh(2), S.ring_scenario(dt=0.5), 1)
+    st0 = disc.project_initial()
+    assert rel_l2(disc.compute_lambda(st0, 0.0), g["lam"]) < TOL
+    out = disc.run(st0, t_end=1.0)
+    assert field_rel(out.c, g["c2"]) < TOL
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_lake_at_rest_vs_reference(golden, k):
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    g = golden(f"lake_k{k}.npz")
+    disc = _disc(M.build_square_mesh(2, 0.2, 5), S.lake_at_rest_scenario(dt=0.5), k)
+    st0 = disc.project_initial()
+    assert np.abs(disc.rhs(st0, 0.0)).max() < 1e-10
+    out = disc.run(st0, t_end=5.0)
+    assert np.abs(out.c - g["c10"]).max() < 1e-9
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_walls_and_p4_vs_oracle(k):
+    """Unpinned extensions (walls, p=4) against the dense CPU oracle."""
+    from oracle import qfswe_oracle as O
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    mesh = M.build_unit_square_mesh(8)
+    p = S.bump_scenario(seed=0, dt=2e-4, cfl=None)
+    o = O.OScenario(dt=2e-4, dirichlet_markers=frozenset(), wall_markers=frozenset({1}),
+                    hb=p.hb, initial=p.initial)
+    disc = _disc(mesh, p, k)
+    orc = O.OracleSolver(O.OMesh(mesh.vertices, mesh.triangles), o, k)
+    c0, u0 = orc.project_initial()
+    st0 = disc.project_initial()
+    assert field_rel(st0.c, c0) < TOL
+    assert field_rel(disc.rhs(st0, 0.0), orc.rhs(c0, u0, 0.0)) < 1e-10
+    out = disc.run(st0, t_end=10 * 2e-4)
+    ref, _, _ = orc.run(c0, 0.0, 10)
+    assert field_rel(out.c, ref) < TOL
+
+
+def test_p4_mms_vs_oracle():
+    from oracle import qfswe_oracle as O
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    mesh = M.build_unit_square_mesh(4)
+    disc = _disc(mesh, S.mms_scenario(dt=2e-5), 4)
+    orc = O.OracleSolver(O.OMesh(mesh.vertices, mesh.triangles), O.mms_baseline(dt=2e-5), 4)
+    c0, u0 = orc.project_initial()
+    st0 = disc.project_initial()
+    assert field_rel(st0.c, c0) < TOL
+    assert field_rel(disc.rhs(st0, 0.01), orc.rhs(c0, u0, 0.01)) < TOL
+    out = disc.run(st0, t_end=5 * 2e-5)
+    ref, _, _ = orc.run(c0, 0.0, 5)
+    assert field_rel(out.c, ref) < TOL
