@@ -1,0 +1,345 @@
+"""Benchmark: DG DoF-updates/s per RK stage on B200 (BASELINE.json metric).
+
+Default workload = BASELINE configs[1] (C2): manufactured solution, p = 2,
+2 x 256 x 256 = 131,072 triangles of the unit square, SSP-RK3, dt = 2e-5.
+A "step" is one SSP-RK3 step = 3 stages; one DoF-update is one modal
+coefficient of (xi, U, V) advanced through one stage (3*K*E per stage).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5]
+    python bench.py --impl reference ...   # CPU oracle port on the host cores
+
+Timing: CUDA events on the launching stream around each step, max over
+ranks; the 131k-element C2 state (19 MB) fits in L2, so L2 is flushed
+(a 256 MB write) between timed steps and the flush is outside the events.
+Per-stage events also time the dominant kernel (stage_kernel) for the
+roofline.  ``e2e`` is measured through ``Discretization.step`` with host
+(numpy) states: H2D of c, step, D2H of (c, u) every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (order, n, scenario, dt or None (CFL), jitter, description)
+    "c1": (1, 32, "mms", 1e-4, 0.0, "C1 MMS p=1 N=32 SSP-RK2 dt=1e-4"),
+    "c2": (2, 256, "mms", 2e-5, 0.0, "C2 MMS p=2 N=256 SSP-RK3 dt=2e-5"),
+    "c3": (3, 1024, "bumps", None, 0.0, "C3 bumps+walls p=3 N=1024 SSP-RK3 CFL 0.1"),
+    "c4": (2, 2048, "bumps", None, 0.2, "C4 jittered bumps+walls p=2 N=2048 SSP-RK3 CFL 0.1"),
+    "c5": (4, 1448, "bumps", None, 0.0, "C5 weak bumps+walls p=4 N=1448/GPU SSP-RK3 CFL 0.1"),
+}
+METRIC = "DG DoF-updates/s per RK stage (p=1..4) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stages_of(k):
+    return 1 if k == 0 else (2 if k == 1 else 3)
+
+
+def rk_coeffs(k):
+    if k == 0:
+        return [(0.0, 1.0, 0.0)]
+    if k == 1:
+        return [(0.0, 1.0, 0.0), (0.5, 0.5, 1.0)]
+    return [(0.0, 1.0, 0.0), (0.75, 0.25, 1.0), (1.0 / 3.0, 2.0 / 3.0, 0.5)]
+
+
+def alg_bytes_per_elem(K, r):
+    """read c, write c_out, (+ read c0), + 64 B static + 12 B ids."""
+    return 8 * 3 * K * (2 + r) + 64 + 12
+
+
+def build_problem(cfg, n_override=None):
+    from paper_1904_08684_b200 import mesh as M
+    from paper_1904_08684_b200 import scenario as S
+
+    k, n, scen, dt, jit, _ = CONFIGS[cfg]
+    n = n_override or n
+    mesh = M.build_unit_square_mesh(n, jitter=jit, seed=7) if jit else M.build_unit_square_mesh(n)
+    if scen == "mms":
+        scn = S.mms_scenario(dt=dt)
+    else:
+        scn = S.bump_scenario(seed=0, cfl=0.1)
+    return k, n, mesh, scn
+
+
+class Clocks:
+    """SM clock + throttle reasons sampled through NVML during the timed
+    region (the B200_PROFILING.md clocks line; nvidia-smi's 100 ms sampling
+    is too coarse for a few-ms region, so one sample is taken per step)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, idx):
+        self.samples, self.reasons, self.h = [], set(), None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.h = None
+
+    def sample(self):
+        if self.h is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def stop(self):
+        if self.h is None or not self.samples:
+            return None
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max),
+                "samples": len(self.samples), "reasons": sorted(self.reasons), "source": "nvml"}
+
+
+def cpu_baseline(cfg, budget_s=12.0, n_sample=64, max_steps=None, threads="all"):
+    """Oracle port (dense NumPy restatement of the reference) on this host."""
+    from oracle import qfswe_oracle as O
+
+    k, n, mesh, scn = build_problem(cfg, n_override=n_sample)
+    if scn.name == "mms":
+        oscn = O.mms_baseline(dt=scn.dt)
+    else:
+        oscn = O.OScenario(dt=1e-4, dirichlet_markers=frozenset(), wall_markers=frozenset({1}),
+                           hb=scn.hb, initial=scn.initial)
+    orc = O.OracleSolver(O.OMesh(mesh.vertices, mesh.triangles), oscn, k)
+    c, _ = orc.project_initial()
+    if scn.cfl is not None:
+        _, u = orc.project_initial()
+        orc.dt = orc.cfl_dt(scn.cfl, c, u)
+    orc.step(c, 0.0)  # warm-up
+    t0 = time.perf_counter()
+    steps, t = 0, 0.0
+    while True:
+        c, _, t = orc.step(c, t)
+        steps += 1
+        el = time.perf_counter() - t0
+        if (max_steps and steps >= max_steps) or (not max_steps and el >= budget_s):
+            break
+    K = orc.K
+    dof = 3 * K * mesh.n_triangles * stages_of(k) * steps
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": dof / el, "unit": "DoF-updates/s", "cores": int(cores), "kind": "port",
+            "sample": f"{CONFIGS[cfg][5]} restricted to N={n_sample} "
+                      f"({mesh.n_triangles} elements), {steps} steps, wall clock, "
+                      f"{os.cpu_count()} host cores visible", "elapsed_s": el}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.config, max_steps=1)  # one step probe
+    per_step = cb["elapsed_s"]
+    k, n, _, _ = build_problem(args.config)
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        pass
+    cbw = cpu_baseline(args.config, max_steps=max(args.steps, 1))
+    line = {
+        "metric": METRIC, "value": cbw["value"], "unit": "DoF-updates/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cbw["elapsed_s"] / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": CONFIGS[args.config][5], "order": k, "n": n,
+                   "sample_n": 64, "parallelism": "host cores (NumPy/OpenBLAS)"},
+        "cpu_baseline": {k_: cbw[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cbw["value"], "unit": "DoF-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "probe_step_s": per_step, "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+
+    from paper_1904_08684_b200 import _cabi
+    from paper_1904_08684_b200.solver import Discretization, State
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+        from paper_1904_08684_b200 import distributed as QD
+        return QD.bench_distributed(args, CONFIGS, METRIC)
+    lib = _cabi.load()
+    k, n, mesh, scn = build_problem(args.config, args.n)
+    disc = Discretization(mesh, scn, k)
+    st0 = disc.project_initial()
+    K, E, ld = disc.K, mesh.n_triangles, disc.ld
+    ds = disc.to_device(st0)
+    ds.t_dev[1] = disc.dt
+    work = disc._work_buf()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
+    S5, S3 = 5 * K * ld, 3 * K * ld
+    c1, u1 = work[:S3], work[S3:S5]
+    c2, u2 = work[S5:S5 + S3], work[S5 + S3:]
+    coeffs = rk_coeffs(k)
+    bufs = {0: (ds.c, ds.u), 1: (c1, u1), 2: (c2, u2)}
+    plan = [(0, 1), (1, 2), (2, 0)] if k >= 2 else ([(0, 1), (1, 0)] if k == 1 else [(0, 1)])
+
+    has_bnd = disc.tables.bnd_elem.size > 0
+    dt = disc.dt
+    tnow = [st0.t]
+
+    def one_step(evs=None):
+        t = tnow[0]
+        for si, ((src, dst), (a, b, toff)) in enumerate(zip(plan, coeffs)):
+            ts = t + toff * dt
+            if has_bnd:
+                _cabi.check(lib.qf_ghost(disc._ctx, ts, sp), "qf_ghost")
+            ci, ui = bufs[src]
+            co, uo = bufs[dst]
+            if evs is not None:
+                evs[si][0].record(stream)
+            _cabi.check(lib.qf_stage(disc._ctx, ci.data_ptr(), ui.data_ptr(), ds.c.data_ptr(),
+                                     co.data_ptr(), uo.data_ptr(), a, b, ts, dt, None, 0.0, 0,
+                                     -1, sp), "qf_stage")
+            if evs is not None:
+                evs[si][1].record(stream)
+        if k == 0:
+            ds.c.copy_(c1)
+            ds.u.copy_(u1)
+        tnow[0] = t + dt
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    n0 = lib.qf_launch_count()
+    step_ms, stage_ms = [], []
+    for it in range(args.steps):
+        flush.fill_(float(it))  # L2 flush outside the timed events
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in plan]
+        ev0.record(stream)
+        one_step(evs)
+        ev1.record(stream)
+        clocks.sample()
+        torch.cuda.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        stage_ms.append([a.elapsed_time(b) for a, b in evs])
+    launches = lib.qf_launch_count() - n0
+    clk = clocks.stop()
+    disc._raise_errors("bench")
+    total_ms = float(np.sum(step_ms))
+    ns = stages_of(k)
+    dof = 3 * K * E * ns * args.steps
+    value = dof / (total_ms * 1e-3)
+    # roofline of the dominant kernel (stage_kernel), algorithmic bytes
+    peak, peak_src = peaks()
+    st = np.array(stage_ms)  # (steps, stages)
+    rvec = [0] + [1] * (ns - 1)
+    bytes_step = sum(E * alg_bytes_per_elem(K, r) for r in rvec)
+    kern_ms = float(st.sum())
+    achieved = bytes_step * args.steps / (kern_ms * 1e-3) / 1e9
+    # e2e: public API with host states (H2D c, step, D2H c and u)
+    e2e = measure_e2e(disc, st0, max(3, min(args.steps, 20)))
+    cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][5], "order": k, "n": n, "elements": E,
+                   "K": K, "stages_per_step": ns, "dt": disc.dt,
+                   "dof_per_stage": 3 * K * E, "l2": "flushed (256 MB write) between timed steps",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "stage_kernel", "kernel_ms_per_step": kern_ms / args.steps,
+                     "alg_bytes_per_step": bytes_step,
+                     "kernel_share_of_step": kern_ms / total_ms},
+        "hbm_roofline_dof_per_s": 3 * K * E * ns / (bytes_step / (peak * 1e9)),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    line["roofline_frac_dof"] = value / line["hbm_roofline_dof_per_s"]
+    if cb is not None:
+        line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+
+
+def measure_e2e(disc, st0, steps):
+    """Discretization.step with host states: H2D(c) + step + D2H(c, u) per step."""
+    import torch
+
+    from paper_1904_08684_b200.solver import State
+
+    st = State(st0.c.copy(), st0.u.copy(), st0.t)
+    E, K = disc.mesh.n_triangles, disc.K
+    st = disc.step(st)
+    _ = st.c
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = disc.step(State(st.c, st.u, st.t))
+        _ = st.c  # D2H of (c, u)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    ns = stages_of(disc.k)
+    return {"value": 3 * K * E * ns * steps / el, "unit": "DoF-updates/s",
+            "h2d_bytes_per_step": 8 * 3 * K * E, "d2h_bytes_per_step": 8 * 5 * K * E,
+            "timing": "wall clock around Discretization.step with numpy states"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override mesh resolution")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -12,6 +12,8 @@ namespace qf {
 
 template <int k>
 struct Ord;
+template <int k>
+struct Tabs;
 
 constexpr double TWO_PI = 6.283185307179586;
 
@@ -31,8 +33,18 @@ struct Tab {
 struct Phys {
   double g, fc, tau;
   int hb_linear, kind, forcing;
+  int taylor;  // element-local Taylor sincos for the MMS forcing (|2 pi dx| <= 0.06)
   double p[8];
 };
+
+// sin / cos of a small angle z (|z| <= 0.06): truncation < 1e-19 relative
+__device__ __forceinline__ void sincos_small(double z, double& s, double& c) {
+  const double z2 = z * z;
+  s = z * fma(z2, fma(z2, fma(z2, fma(z2, 2.7557319223985893e-06, -1.984126984126984e-04),
+                                   8.333333333333333e-03), -1.6666666666666666e-01), 1.0);
+  c = fma(z2, fma(z2, fma(z2, fma(z2, 2.48015873015873e-05, -1.388888888888889e-03),
+                               4.1666666666666664e-02), -0.5), 1.0);
+}
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
@@ -82,6 +94,27 @@ __device__ __forceinline__ void flux_forcing(const Phys& P, double H, double Hx,
 // Volume source of the family at (x, y): S (xi mass source), Fx, Fy.
 // (st, ct) = (sin 2 pi t, cos 2 pi t) for MMS; the spatial phases use two
 // sincospi per point and angle addition.
+// MMS: (sx, cx, sy, cy) = sin/cos(2 pi x), sin/cos(2 pi y) supplied by the caller.
+__device__ __forceinline__ void forcing_mms(const Phys& P, double x, double y, double sx,
+                                            double cx, double sy, double cy, double st, double ct,
+                                            double& S, double& Fx, double& Fy) {
+    const double A = P.p[4], au = P.p[5], av = P.p[6];
+    const double s2 = sx * ct - cx * st, c2 = cx * ct + sx * st;  // 2 pi (x - t)
+    const double s3 = sy * ct - cy * st, c3 = cy * ct + sy * st;  // 2 pi (y - t)
+    const double sxy = sx * cy + cx * sy, cxy = cx * cy - sx * sy;
+    const double s1 = sxy * ct - cxy * st, c1 = cxy * ct + sxy * st;  // 2 pi (x + y - t)
+    const double xi = A * s1, xd = TWO_PI * A * c1;                  // xi_x = xi_y = -xi_t
+    const double u = au * c2, ux = -TWO_PI * au * s2;                  // u_t = -u_x
+    const double v = av * s3, vy = TWO_PI * av * c3;                   // v_t = -v_y
+    const double H = hb_exact(P, x, y) + xi;
+    const double Hx = P.p[1] + P.p[3] * y + xd, Hy = P.p[2] + P.p[3] * x + xd, Ht = -xd;
+    const double U = H * u, V = H * v;
+    const double Ut = Ht * u - H * ux, Ux = Hx * u + H * ux, Uy = Hy * u;
+    const double Vt = Ht * v - H * vy, Vx = Hx * v, Vy = Hy * v + H * vy;
+    S = -xd + Ux + Vy;
+    flux_forcing(P, H, Hx, Hy, U, Ut, Ux, Uy, V, Vt, Vx, Vy, xd, xd, Fx, Fy);
+}
+
 __device__ __forceinline__ void forcing(const Phys& P, double x, double y, double t, double st,
                                         double ct, double& S, double& Fx, double& Fy) {
   if (P.kind == SCN_MMS) {
@@ -117,69 +150,6 @@ __device__ __forceinline__ void forcing(const Phys& P, double x, double y, doubl
   } else {
     S = Fx = Fy = 0.0;
   }
-}
-
-// ------------------------------------------------- velocity (Eq. 12)
-// A = sum_i H_i G[:, i, :] (times 1/sqrt(detB)); LDL^T without pivoting
-// (A is SPD when H > 0; matches the reference's LU, solver.py:315-336, to
-// roundoff), u = sqrt(detB) A^-1 q.  Returns false on a zero/non-finite
-// pivot or non-finite result (SingularProjection, solver.py:330-335).
-template <int k>
-__device__ __forceinline__ bool solve_velocity(const double* xi, const double* qU,
-                                               const double* qV, const double* hb, double sd,
-                                               double* uo, double* vo) {
-  using O = Ord<k>;
-  constexpr int K = O::K;
-  double H[K];
-#pragma unroll
-  for (int i = 0; i < K; ++i) H[i] = xi[i] + hb[i];
-  double A[K * (K + 1) / 2];
-  O::vel_matrix(H, A);
-#define QF_A(p, m) A[(m) * ((m) + 1) / 2 + (p)]
-  bool ok = true;
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const double d = QF_A(j, j);
-    ok = ok && (d != 0.0) && isfinite(d);
-    const double id = 1.0 / d;
-#pragma unroll
-    for (int i = j + 1; i < K; ++i) {
-      const double l = QF_A(j, i) * id;
-#pragma unroll
-      for (int m = i; m < K; ++m) QF_A(i, m) = fma(-l, QF_A(j, m), QF_A(i, m));
-      QF_A(j, i) = l;
-    }
-    QF_A(j, j) = id;
-  }
-  // forward (unit lower), diagonal, backward
-  double y1[K], y2[K];
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    double a = qU[i], b = qV[i];
-#pragma unroll
-    for (int j = 0; j < i; ++j) {
-      a = fma(-QF_A(j, i), y1[j], a);
-      b = fma(-QF_A(j, i), y2[j], b);
-    }
-    y1[i] = a;
-    y2[i] = b;
-  }
-#pragma unroll
-  for (int i = K - 1; i >= 0; --i) {
-    double a = y1[i] * QF_A(i, i), b = y2[i] * QF_A(i, i);
-#pragma unroll
-    for (int m = i + 1; m < K; ++m) {
-      a = fma(-QF_A(i, m), y1[m], a);
-      b = fma(-QF_A(i, m), y2[m], b);
-    }
-    y1[i] = a;
-    y2[i] = b;
-    uo[i] = sd * a;
-    vo[i] = sd * b;
-    ok = ok && isfinite(a) && isfinite(b);
-  }
-#undef QF_A
-  return ok;
 }
 
 }  // namespace qf

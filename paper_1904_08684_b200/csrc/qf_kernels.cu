@@ -49,34 +49,47 @@ struct StageArgs {
 };
 
 // ---------------------------------------------------------------- edges
-template <int k, int J>
+// One local edge j (runtime, loop not unrolled to keep the kernel inside the
+// instruction cache); Lambda comes from the shared-memory copy of the
+// per-order table (uniform j -> broadcast, neighbour j' -> at most 3 rows).
+template <int k>
+__device__ __forceinline__ void trace_s(const double* __restrict__ sL, int j, const double* f,
+                                        double scale, double* t) {
+  constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
+  const double* L = sL + j * K * NT;
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc = fma(L[i * NT + a], f[i], acc);
+    t[a] = acc * scale;
+  }
+}
+
+template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
-                                          const double* c, const double* u, const double* hb,
-                                          double B11, double B12, double B21, double B22,
-                                          double sd, double isd, double* r) {
+                                          int j, const double* __restrict__ sL, const double* c,
+                                          const double* u, const double* hb, double B11,
+                                          double B12, double B21, double B22, double isd,
+                                          double* r) {
   using O = Ord<k>;
   constexpr int K = O::K, NT = O::NT, NH = O::NH;
   const int64_t ld = T.ld;
   // own outward normal: physical image of the reference edge direction
-  constexpr double d1 = J == 0 ? -1.0 : (J == 1 ? 0.0 : 1.0);
-  constexpr double d2 = J == 0 ? 1.0 : (J == 1 ? -1.0 : 0.0);
+  const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
+  const double d2 = j == 0 ? 1.0 : (j == 1 ? -1.0 : 0.0);
   const double dx = B11 * d1 + B12 * d2, dy = B21 * d1 + B22 * d2;
   const double ln = sqrt(dx * dx + dy * dy);
   const double n1 = dy / ln, n2 = -dx / ln;
 
   double own[6][NT], oth[6][NT];
 #pragma unroll
-  for (int f = 0; f < 5; ++f) {
-    O::template trace<J>(f < 3 ? c + f * K : u + (f - 3) * K, own[f]);
-#pragma unroll
-    for (int a = 0; a < NT; ++a) own[f][a] *= isd;
-  }
-  O::template trace<J>(hb, own[5]);
-#pragma unroll
-  for (int a = 0; a < NT; ++a) own[5][a] *= isd;
-  double hbm_o = hb[0] * isd * 0.7071067811865476, hbm_n = hbm_o;
+  for (int f = 0; f < 5; ++f) trace_s<k>(sL, j, f < 3 ? c + f * K : u + (f - 3) * K, isd, own[f]);
+  trace_s<k>(sL, j, hb, isd, own[5]);
+  const double hbm_o = hb[0] * isd * 0.7071067811865476;
+  double hbm_n = hbm_o;
 
-  const int code = T.nbr[J * ld + e];
+  const int code = T.nbr[j * ld + e];
   bool dirichlet = false;
   const double* gp = nullptr;
   if (code >= 0) {
@@ -96,9 +109,9 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
         for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
         hbm_n = f[0] * nisd * 0.7071067811865476;
       }
-      O::trace_dyn(jn, f, oth[fi]);
+      trace_s<k>(sL, jn, f, nisd, oth[fi]);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) oth[fi][a] *= (a & 1) ? -nisd : nisd;  // s -> 1-s
+      for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
     }
   } else {
     const int v = -1 - code, slot = v >> 1;
@@ -159,7 +172,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     hmin = fmin(hmin, sH[s]);
   }
   if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
-  if (A.lam) A.lam[J * ld + e] = lam;
+  if (A.lam) A.lam[j * ld + e] = lam;
 
   // Lax-Friedrichs flux in trace space (reference solver.py:610-613)
   double wO[NT], wN[NT], pO[NT], pN[NT], aO[NT], aN[NT], bO[NT], bN[NT];
@@ -174,29 +187,50 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   O::jprod(oth[1], unN, aN);
   O::jprod(own[2], unO, bO);
   O::jprod(oth[2], unN, bN);
-  double Fx[NT], FU[NT], FV[NT];
+  double F[3][NT];
   const double hl = 0.5 * lam, g = P.g;
 #pragma unroll
   for (int a = 0; a < NT; ++a) {
     double pr = pO[a] + pN[a];
     if (!P.hb_linear) pr += hbm_o * own[0][a] + hbm_n * oth[0][a];
-    Fx[a] = 0.5 * (n1 * (own[1][a] + oth[1][a]) + n2 * (own[2][a] + oth[2][a])) +
-            hl * (own[0][a] - oth[0][a]);
-    FU[a] = 0.5 * (aO[a] + aN[a] + g * n1 * pr) + hl * (own[1][a] - oth[1][a]);
-    FV[a] = 0.5 * (bO[a] + bN[a] + g * n2 * pr) + hl * (own[2][a] - oth[2][a]);
+    F[0][a] = 0.5 * (n1 * (own[1][a] + oth[1][a]) + n2 * (own[2][a] + oth[2][a])) +
+              hl * (own[0][a] - oth[0][a]);
+    F[1][a] = 0.5 * (aO[a] + aN[a] + g * n1 * pr) + hl * (own[1][a] - oth[1][a]);
+    F[2][a] = 0.5 * (bO[a] + bN[a] + g * n2 * pr) + hl * (own[2][a] - oth[2][a]);
   }
+  // lift: r_f[p] -= (len / sqrt(detB)) sum_a Lambda_j[p, a] F_f[a]
   const double s = ln * isd;
-  O::template lift<J>(Fx, s, r);
-  O::template lift<J>(FU, s, r + K);
-  O::template lift<J>(FV, s, r + 2 * K);
-  (void)sd;
+  const double* L = sL + j * K * NT;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) {
+      const double w = L[p * NT + a];
+      l0 = fma(w, F[0][a], l0);
+      l1 = fma(w, F[1][a], l1);
+      l2 = fma(w, F[2][a], l2);
+    }
+    r[p] = fma(-s, l0, r[p]);
+    r[K + p] = fma(-s, l1, r[K + p]);
+    r[2 * K + p] = fma(-s, l2, r[2 * K + p]);
+  }
 }
+
+template <int k>
+struct Occ {
+  static constexpr int value = k <= 1 ? 4 : (k == 2 ? 3 : (k == 3 ? 2 : 1));
+};
 
 // ---------------------------------------------------------- stage kernel
 template <int k>
-__global__ void __launch_bounds__(128) stage_kernel(Tab T, Phys P, StageArgs A) {
+__global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
-  constexpr int K = O::K, NH = O::NH;
+  using TB = Tabs<k>;
+  constexpr int K = O::K, NH = O::NH, NQ = O::NQ;
+  __shared__ double s_tab[TB::SIZE];
+  for (int i = threadIdx.x; i < TB::SIZE; i += blockDim.x) s_tab[i] = TB::ptr()[i];
+  __syncthreads();
   const int e = A.e0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= A.e0 + A.n) return;
   const int64_t ld = T.ld;
@@ -273,26 +307,53 @@ __global__ void __launch_bounds__(128) stage_kernel(Tab T, Phys P, StageArgs A) 
       r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
       r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
     }
-    if (P.forcing) {
+    if (P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
       const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
       double st, ct;
       sincospi(2.0 * t, &st, &ct);
-      O::quad_project(
-          [&](double x1, double x2, double& f0, double& f1, double& f2) {
-            const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
-            double S, Fx, Fy;
-            forcing(P, x, y, t, st, ct, S, Fx, Fy);
-            f0 = sd * S;
-            f1 = sd * Fx;
-            f2 = sd * Fy;
-          },
-          r, r + K, r + 2 * K);
+      // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
+      // value by a Taylor-evaluated small angle (2 sincospi per element
+      // instead of 2 per quadrature point)
+      const bool tay = P.kind == SCN_MMS && P.taylor;
+      const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
+      double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0;
+      if (tay) {
+        sincospi(2.0 * x0, &sx0, &cx0);
+        sincospi(2.0 * y0, &sy0, &cy0);
+      }
+#pragma unroll 1
+      for (int q = 0; q < NQ; ++q) {
+        const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
+        const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+        double S, Fx, Fy;
+        if (tay) {
+          const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
+          double sz, cz, sw, cw;
+          sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+          sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+          forcing_mms(P, x, y, fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz),
+                      fma(sy0, cw, cy0 * sw), fma(cy0, cw, -sy0 * sw), st, ct, S, Fx, Fy);
+        } else {
+          forcing(P, x, y, t, st, ct, S, Fx, Fy);
+        }
+        S *= sd;
+        Fx *= sd;
+        Fy *= sd;
+        const double* Pq = s_tab + TB::P + q * K;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const double w = Pq[p];
+          r[p] = fma(w, S, r[p]);
+          r[K + p] = fma(w, Fx, r[K + p]);
+          r[2 * K + p] = fma(w, Fy, r[2 * K + p]);
+        }
+      }
     }
   }
   if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
-    edge_term<k, 0>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
-    edge_term<k, 1>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
-    edge_term<k, 2>(T, P, A, e, c, u, hb, B11, B12, B21, B22, sd, isd, r);
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j)
+      edge_term<k>(T, P, A, e, j, s_tab + TB::L, c, u, hb, B11, B12, B21, B22, isd, r);
   }
   if (A.mode == 0) {
 #pragma unroll
@@ -311,8 +372,10 @@ __global__ void __launch_bounds__(128) stage_kernel(Tab T, Phys P, StageArgs A) 
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = c[i];
   if (!fin) atomicOr(A.err, BIT_NONFINITE);
-  double uo[K], vo[K];
-  if (!solve_velocity<k>(c, c + K, c + 2 * K, hb, sd, uo, vo)) atomicOr(A.err, BIT_SINGULAR);
+  double H[K], uo[K], vo[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) H[i] = c[i] + hb[i];
+  if (!O::vel_solve(H, c + K, c + 2 * K, sd, uo, vo)) atomicOr(A.err, BIT_SINGULAR);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     A.u_out[i * ld + e] = uo[i];
@@ -337,7 +400,10 @@ __global__ void __launch_bounds__(128)
   for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
 #pragma unroll
   for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
-  if (!solve_velocity<k>(cc, cc + K, cc + 2 * K, hb, sd, uo, vo)) atomicOr(err, BIT_SINGULAR);
+  double H[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) H[i] = cc[i] + hb[i];
+  if (!O::vel_solve(H, cc + K, cc + 2 * K, sd, uo, vo)) atomicOr(err, BIT_SINGULAR);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     u[i * ld + e] = uo[i];
@@ -525,6 +591,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
   x->phys.hb_linear = d->hb_linear;
   x->phys.kind = d->scn_kind;
   x->phys.forcing = d->has_forcing;
+  x->phys.taylor = d->taylor;
   for (int i = 0; i < 8; ++i) x->phys.p[i] = d->scn_params[i];
   if (cudaMalloc(&x->err, sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {

@@ -215,12 +215,20 @@ class Discretization:
         for i, p in enumerate(scn.device.as_array()):
             d.scn_params[i] = float(p)
         d.has_forcing = 1 if (scn.forcing is not None or scn.mass_source is not None) else 0
+        d.taylor = 1 if self._max_quad_angle() <= 0.06 else 0
         self._desc = d
         ctx = _cabi.C.c_void_p()
         _cabi.check(lib.qf_create(_cabi.C.byref(d), _cabi.C.byref(ctx)), "qf_create")
         self._ctx = ctx
         self._lib = lib
         self._work = None
+
+    def _max_quad_angle(self) -> float:
+        """max |2 pi (x_q - x_centroid)| over quadrature points (MMS Taylor gate)."""
+        B = self.geom.B
+        r = self.quad_ref - 1.0 / 3.0
+        d = np.abs(np.einsum("eab,qb->eqa", B, r)).max() if len(B) else 0.0
+        return 2.0 * math.pi * float(d)
 
     def __del__(self):
         try:
