@@ -61,7 +61,7 @@ typedef struct qf_desc {
   int32_t n_bnd;            /* Dirichlet boundary slots */
   const int32_t* bnd_elem;  /* [n_bnd] */
   const int32_t* bnd_local; /* [n_bnd] */
-  double* ghost;            /* [n_bnd][5*(k+1)+6] scratch, written per stage */
+  double* ghost;            /* [3][n_bnd][5*(k+2)+6] scratch: exact data per RK stage */
   /* physics (scenario.py:34-49) */
   double g, f_c, tau_bf;
   int32_t hb_linear;        /* hb_mode == "linear" */
@@ -83,7 +83,8 @@ void qf_destroy(qf_ctx* ctx);
  * [e0, e0+n) of state c (n < 0: all owned elements). */
 int qf_velocity(qf_ctx* ctx, const double* c, double* u, int32_t e0, int32_t n, void* stream);
 
-/* Dirichlet ghost traces at time t (solver.py:395-402, 636-653). */
+/* Dirichlet ghost data at time t into stage table 0 (solver.py:395-402, 636-653);
+ * qf_stage reads table 0, qf_step/qf_run fill all stage tables themselves. */
 int qf_ghost(qf_ctx* ctx, double t, void* stream);
 
 /* Discretization.rhs / element_rhs / edge_rhs / source_rhs / compute_lambda

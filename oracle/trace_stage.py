@@ -266,6 +266,15 @@ class TraceStage:
         for f, F in enumerate((Fx, FU, FV)):
             out[f] -= s * (L @ F)
 
+    def stage_coeffs(self, a, b, c_in, u_in, c0, t, dt):
+        """c_out = a c0 + b (c_in + dt L(c_in)) for owned elements, and its velocity."""
+        n = self.n
+        r = self.rhs(c_in, u_in, t)
+        cn = a * c0[:, :, :n] + b * (c_in[:, :, :n] + dt * r)
+        full = c_in.copy()
+        full[:, :, :n] = cn
+        return cn, self.velocity(full)
+
     def stage(self, s, c_in, u_in, c0, t, dt):
         """SSP-RK stage s (1-based) for order k; returns (c_out, u_out) owned part."""
         k = self.k

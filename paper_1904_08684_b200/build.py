@@ -45,7 +45,7 @@ def _digest() -> str:
     for p in _sources():
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(" ".join(NVCC_FLAGS).encode())
+    h.update(" ".join(NVCC_FLAGS + os.environ.get("QF_NVCC_EXTRA", "").split()).encode())
     return h.hexdigest()
 
 
@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     dig = _digest()
     if not force and LIB.exists() and stamp.exists() and stamp.read_text() == dig:
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB), str(CSRC / "qf_kernels.cu")]
+    extra = os.environ.get("QF_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(LIB), str(CSRC / "qf_kernels.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

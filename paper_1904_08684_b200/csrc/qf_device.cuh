@@ -26,8 +26,9 @@ struct Tab {
   const double* __restrict__ geo;    // [6][ld]
   const double* __restrict__ hb;     // [NH][ld]
   const int* __restrict__ nbr;       // [3][ld]
-  const double* __restrict__ ghost;  // [n_bnd][5*NT+6]
+  const double* __restrict__ ghost;  // [stage][n_bnd][5*NG+6] raw exact data
   int64_t ld;
+  int n_bnd;
 };
 
 struct Phys {
@@ -94,48 +95,36 @@ __device__ __forceinline__ void flux_forcing(const Phys& P, double H, double Hx,
 // Volume source of the family at (x, y): S (xi mass source), Fx, Fy.
 // (st, ct) = (sin 2 pi t, cos 2 pi t) for MMS; the spatial phases use two
 // sincospi per point and angle addition.
-// MMS: (sx, cx, sy, cy) = sin/cos(2 pi x), sin/cos(2 pi y) supplied by the caller.
-__device__ __forceinline__ void forcing_mms(const Phys& P, double x, double y, double sx,
-                                            double cx, double sy, double cy, double st, double ct,
-                                            double& S, double& Fx, double& Fy) {
-    const double A = P.p[4], au = P.p[5], av = P.p[6];
-    const double s2 = sx * ct - cx * st, c2 = cx * ct + sx * st;  // 2 pi (x - t)
-    const double s3 = sy * ct - cy * st, c3 = cy * ct + sy * st;  // 2 pi (y - t)
-    const double sxy = sx * cy + cx * sy, cxy = cx * cy - sx * sy;
-    const double s1 = sxy * ct - cxy * st, c1 = cxy * ct + sxy * st;  // 2 pi (x + y - t)
-    const double xi = A * s1, xd = TWO_PI * A * c1;                  // xi_x = xi_y = -xi_t
-    const double u = au * c2, ux = -TWO_PI * au * s2;                  // u_t = -u_x
-    const double v = av * s3, vy = TWO_PI * av * c3;                   // v_t = -v_y
-    const double H = hb_exact(P, x, y) + xi;
-    const double Hx = P.p[1] + P.p[3] * y + xd, Hy = P.p[2] + P.p[3] * x + xd, Ht = -xd;
-    const double U = H * u, V = H * v;
-    const double Ut = Ht * u - H * ux, Ux = Hx * u + H * ux, Uy = Hy * u;
-    const double Vt = Ht * v - H * vy, Vx = Hx * v, Vy = Hy * v + H * vy;
-    S = -xd + Ux + Vy;
-    flux_forcing(P, H, Hx, Hy, U, Ut, Ux, Uy, V, Vt, Vx, Vy, xd, xd, Fx, Fy);
+// MMS from element-local phases: (s2,c2) = sin/cos 2pi(x-t), (s3,c3) =
+// sin/cos 2pi(y-t), (s1,c1) = sin/cos 2pi(x+y-t).  With U = H u, V = H v the
+// reference's manufactured forcing (scenario.py:78-93) is division-free:
+//   Fx = u D + H (u_t + 2 u u_x + u v_y + g xi_x),
+//   Fy = v D + H (v_t + u_x v + 2 v v_y + g xi_y),   D = H_t + u H_x + v H_y,
+//   S  = xi_t + H_x u + H u_x + H_y v + H v_y   (u_y = v_x = 0).
+__device__ __forceinline__ void forcing_mms(const Phys& P, double x, double y, double s1,
+                                            double c1, double s2, double c2, double s3,
+                                            double c3, double& S, double& Fx, double& Fy) {
+  const double A = P.p[4], au = P.p[5], av = P.p[6];
+  const double xi = A * s1, xd = TWO_PI * A * c1;  // xi_x = xi_y = -xi_t
+  const double u = au * c2, ux = -TWO_PI * au * s2;  // u_t = -u_x
+  const double v = av * s3, vy = TWO_PI * av * c3;   // v_t = -v_y
+  const double H = hb_exact(P, x, y) + xi;
+  const double Hx = P.p[1] + P.p[3] * y + xd, Hy = P.p[2] + P.p[3] * x + xd;
+  const double D = fma(u, Hx, fma(v, Hy, -xd));
+  const double gxd = P.g * xd;
+  Fx = fma(u, D, H * fma(u, fma(2.0, ux, vy), gxd - ux)) + P.tau * H * u - P.fc * H * v;
+  Fy = fma(v, D, H * fma(v, fma(2.0, vy, ux), gxd - vy)) + P.tau * H * v + P.fc * H * u;
+  S = fma(Hx, u, fma(Hy, v, fma(H, ux + vy, -xd)));
 }
 
 __device__ __forceinline__ void forcing(const Phys& P, double x, double y, double t, double st,
                                         double ct, double& S, double& Fx, double& Fy) {
   if (P.kind == SCN_MMS) {
-    const double A = P.p[4], au = P.p[5], av = P.p[6];
-    double sx, cx, sy, cy;
-    sincospi(2.0 * x, &sx, &cx);
-    sincospi(2.0 * y, &sy, &cy);
-    const double s2 = sx * ct - cx * st, c2 = cx * ct + sx * st;  // 2 pi (x - t)
-    const double s3 = sy * ct - cy * st, c3 = cy * ct + sy * st;  // 2 pi (y - t)
-    const double sxy = sx * cy + cx * sy, cxy = cx * cy - sx * sy;
-    const double s1 = sxy * ct - cxy * st, c1 = cxy * ct + sxy * st;  // 2 pi (x + y - t)
-    const double xi = A * s1, xd = TWO_PI * A * c1;                  // xi_x = xi_y = -xi_t
-    const double u = au * c2, ux = -TWO_PI * au * s2;                  // u_t = -u_x
-    const double v = av * s3, vy = TWO_PI * av * c3;                   // v_t = -v_y
-    const double H = hb_exact(P, x, y) + xi;
-    const double Hx = P.p[1] + P.p[3] * y + xd, Hy = P.p[2] + P.p[3] * x + xd, Ht = -xd;
-    const double U = H * u, V = H * v;
-    const double Ut = Ht * u - H * ux, Ux = Hx * u + H * ux, Uy = Hy * u;
-    const double Vt = Ht * v - H * vy, Vx = Hx * v, Vy = Hy * v + H * vy;
-    S = -xd + Ux + Vy;
-    flux_forcing(P, H, Hx, Hy, U, Ut, Ux, Uy, V, Vt, Vx, Vy, xd, xd, Fx, Fy);
+    double s1, c1, s2, c2, s3, c3;
+    sincospi(2.0 * (x + y - t), &s1, &c1);
+    sincospi(2.0 * (x - t), &s2, &c2);
+    sincospi(2.0 * (y - t), &s3, &c3);
+    forcing_mms(P, x, y, s1, c1, s2, c2, s3, c3, S, Fx, Fy);
   } else if (P.kind == SCN_TRAVEL) {
     const double Ca = P.p[4], Ct = P.p[5], ya = P.p[6];
     const double kk = 3.141592653589793 / 600.0;

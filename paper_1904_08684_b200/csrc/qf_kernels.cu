@@ -35,6 +35,14 @@
 
 namespace qf {
 
+// non-CSE'd read-only load: lets a phase re-read its element's data from L1
+// instead of keeping it live in registers across phases
+__device__ __forceinline__ double ldv(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 struct StageArgs {
   const double* __restrict__ c;   // [3][K][ld]
   const double* __restrict__ u;   // [2][K][ld]
@@ -46,6 +54,7 @@ struct StageArgs {
   const double* t_dev;            // optional {t, dt}
   double t, toff, dt, a, b;
   int e0, n, terms, mode;
+  int gstage;                     // Dirichlet ghost table of this stage
 };
 
 // ---------------------------------------------------------------- edges
@@ -66,10 +75,25 @@ __device__ __forceinline__ void trace_s(const double* __restrict__ sL, int j, co
   }
 }
 
+// literal-constant trace / lift of local edge j (switch is warp-uniform for
+// the own side; for the neighbour side it is uniform on warp-homogeneous
+// element orders, see the interleaved thread mapping of stage_kernel)
+template <int k>
+__device__ __forceinline__ void trace_lit(int j, const double* f, double scale, double* t) {
+  using O = Ord<k>;
+  if (j == 0)
+    O::trace0(f, t);
+  else if (j == 1)
+    O::trace1(f, t);
+  else
+    O::trace2(f, t);
+#pragma unroll
+  for (int a = 0; a < O::NT; ++a) t[a] *= scale;
+}
+
 template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
-                                          int j, const double* __restrict__ sL, const double* c,
-                                          const double* u, const double* hb, double B11,
+                                          int j, const double* __restrict__ sL, double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
@@ -79,14 +103,27 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
   const double d2 = j == 0 ? 1.0 : (j == 1 ? -1.0 : 0.0);
   const double dx = B11 * d1 + B12 * d2, dy = B21 * d1 + B22 * d2;
-  const double ln = sqrt(dx * dx + dy * dy);
-  const double n1 = dy / ln, n2 = -dx / ln;
+  const double l2 = dx * dx + dy * dy, il = rsqrt(l2);
+  const double n1 = dy * il, n2 = -dx * il;
 
   double own[6][NT], oth[6][NT];
+  double hbm_o;
+  {
+    double f[K];
 #pragma unroll
-  for (int f = 0; f < 5; ++f) trace_s<k>(sL, j, f < 3 ? c + f * K : u + (f - 3) * K, isd, own[f]);
-  trace_s<k>(sL, j, hb, isd, own[5]);
-  const double hbm_o = hb[0] * isd * 0.7071067811865476;
+    for (int fi = 0; fi < 6; ++fi) {
+      if (fi < 5) {
+        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = ldv(src + i * ld + e);
+      } else {
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
+        hbm_o = f[0] * isd * 0.7071067811865476;
+      }
+      trace_lit<k>(j, f, isd, own[fi]);
+    }
+  }
   double hbm_n = hbm_o;
 
   const int code = T.nbr[j * ld + e];
@@ -96,7 +133,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     const int nb = code >> 2, jn = code & 3;
     const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
     const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
-    const double nisd = 1.0 / sqrt(nB11 * nB22 - nB12 * nB21);
+    const double nisd = rsqrt(nB11 * nB22 - nB12 * nB21);
     double f[K];
 #pragma unroll
     for (int fi = 0; fi < 6; ++fi) {
@@ -109,19 +146,32 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
         for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
         hbm_n = f[0] * nisd * 0.7071067811865476;
       }
-      trace_s<k>(sL, jn, f, nisd, oth[fi]);
+      trace_lit<k>(jn, f, nisd, oth[fi]);
 #pragma unroll
       for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
     }
   } else {
     const int v = -1 - code, slot = v >> 1;
     if ((v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
+      using TB = Tabs<k>;
+      constexpr int NG = O::NG;
       dirichlet = true;
-      gp = T.ghost + (int64_t)slot * (5 * NT + 6);
+      gp = T.ghost + ((int64_t)A.gstage * T.n_bnd + slot) * (5 * NG + 6);
+      const double* gw = sL - TB::L + TB::GPSI;
 #pragma unroll
-      for (int f = 0; f < 5; ++f)
+      for (int f = 0; f < 5; ++f) {
+        double vals[NG];
 #pragma unroll
-        for (int a = 0; a < NT; ++a) oth[f][a] = ldg(gp + f * NT + a);
+        for (int g = 0; g < NG; ++g) vals[g] = ldg(gp + f * NG + g);
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+          double acc = 0.0;
+#pragma unroll
+          for (int g = 0; g < NG; ++g) acc = fma(gw[a * NG + g], vals[g], acc);
+          oth[f][a] = acc;
+        }
+      }
+      gp += 5 * NG - 5 * NT;  // samples follow the raw values
     } else {  // reflective wall: mirror the normal components
 #pragma unroll
       for (int a = 0; a < NT; ++a) {
@@ -146,12 +196,17 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     unN[a] = n1 * oth[3][a] + n2 * oth[4][a];
     tmp[a] = own[5][a] + own[0][a];
   }
+  // sqrt(max(gH, 0)) as x * rsqrt(x): ~1 ulp, identical on both sides of an edge
+  auto wave = [&](double H) {
+    const double x = P.g * H;
+    return x > 0.0 ? x * rsqrt(x) : 0.0;
+  };
   double lam = 0.0, hmin = 1.0;
   O::samples(tmp, sH);
   O::samples(unO, sU);
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    lam = fmax(lam, fabs(sU[s]) + sqrt(fmax(P.g * sH[s], 0.0)));
+    lam = fmax(lam, fabs(sU[s]) + wave(sH[s]));
     hmin = fmin(hmin, sH[s]);
   }
   if (dirichlet) {
@@ -168,7 +223,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   }
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    lam = fmax(lam, fabs(sU[s]) + sqrt(fmax(P.g * sH[s], 0.0)));
+    lam = fmax(lam, fabs(sU[s]) + wave(sH[s]));
     hmin = fmin(hmin, sH[s]);
   }
   if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
@@ -199,27 +254,28 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     F[2][a] = 0.5 * (bO[a] + bN[a] + g * n2 * pr) + hl * (own[2][a] - oth[2][a]);
   }
   // lift: r_f[p] -= (len / sqrt(detB)) sum_a Lambda_j[p, a] F_f[a]
-  const double s = ln * isd;
-  const double* L = sL + j * K * NT;
-#pragma unroll
-  for (int p = 0; p < K; ++p) {
-    double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-#pragma unroll
-    for (int a = 0; a < NT; ++a) {
-      const double w = L[p * NT + a];
-      l0 = fma(w, F[0][a], l0);
-      l1 = fma(w, F[1][a], l1);
-      l2 = fma(w, F[2][a], l2);
-    }
-    r[p] = fma(-s, l0, r[p]);
-    r[K + p] = fma(-s, l1, r[K + p]);
-    r[2 * K + p] = fma(-s, l2, r[2 * K + p]);
+  const double s = l2 * il * isd;  // edge length / sqrt(detB)
+  if (j == 0) {
+    O::lift0(F[0], s, r);
+    O::lift0(F[1], s, r + K);
+    O::lift0(F[2], s, r + 2 * K);
+  } else if (j == 1) {
+    O::lift1(F[0], s, r);
+    O::lift1(F[1], s, r + K);
+    O::lift1(F[2], s, r + 2 * K);
+  } else {
+    O::lift2(F[0], s, r);
+    O::lift2(F[1], s, r + K);
+    O::lift2(F[2], s, r + 2 * K);
   }
 }
 
 template <int k>
 struct Occ {
-  static constexpr int value = k <= 1 ? 4 : (k == 2 ? 3 : (k == 3 ? 2 : 1));
+#ifndef QF_OCC2
+#define QF_OCC2 4
+#endif
+  static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : (k == 3 ? 2 : 1));
 };
 
 // ---------------------------------------------------------- stage kernel
@@ -231,24 +287,35 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
   __shared__ double s_tab[TB::SIZE];
   for (int i = threadIdx.x; i < TB::SIZE; i += blockDim.x) s_tab[i] = TB::ptr()[i];
   __syncthreads();
-  const int e = A.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  // interleaved mapping: warp 2w takes the even, warp 2w+1 the odd elements
+  // of a 64-element tile, so on split-square meshes (element 2q lower, 2q+1
+  // upper triangle of quad q) every warp is homogeneous in its local-edge
+  // pairing and the neighbour trace switch never diverges.
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int e = A.e0 + blockIdx.x * blockDim.x + (wid >> 1) * 64 + 2 * lane + (wid & 1);
   if (e >= A.e0 + A.n) return;
   const int64_t ld = T.ld;
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
   const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
-  const double det = B11 * B22 - B12 * B21, sd = sqrt(det), isd = 1.0 / sd, idet = 1.0 / det;
+  const double det = B11 * B22 - B12 * B21, isd = rsqrt(det), sd = det * isd, idet = isd * isd;
 
-  double c[3 * K], u[2 * K], hb[K], r[3 * K];
-#pragma unroll
-  for (int i = 0; i < 3 * K; ++i) c[i] = ldg(A.c + i * ld + e);
-#pragma unroll
-  for (int i = 0; i < 2 * K; ++i) u[i] = ldg(A.u + i * ld + e);
-#pragma unroll
-  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
+  double r[3 * K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
+  if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j)
+      edge_term<k>(T, P, A, e, j, s_tab + TB::L, B11, B12, B21, B22, isd, r);
+  }
+  double c[3 * K], u[2 * K], hb[K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) c[i] = ldv(A.c + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) u[i] = ldv(A.u + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
   const double* xi = c;
   const double* cU = c + K;
   const double* cV = c + 2 * K;
@@ -263,7 +330,7 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
     O::vol_xi(al, be, ra);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      r[i] = ra[i] * idet;
+      r[i] += ra[i] * idet;
       al[i] = B22 * u[i] - B12 * u[K + i];   // a
       be[i] = -B21 * u[i] + B11 * u[K + i];  // b
       wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
@@ -273,8 +340,8 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
     const double i32 = idet * isd;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      r[K + i] = ra[i] * i32;
-      r[2 * K + i] = rb[i] * i32;
+      r[K + i] += ra[i] * i32;
+      r[2 * K + i] += rb[i] * i32;
     }
     if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
       const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
@@ -315,11 +382,14 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
       // value by a Taylor-evaluated small angle (2 sincospi per element
       // instead of 2 per quadrature point)
       const bool tay = P.kind == SCN_MMS && P.taylor;
+      // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
+      // the centroid; per point only small-angle Taylor rotations follow
       const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
-      double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0;
+      double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
       if (tay) {
-        sincospi(2.0 * x0, &sx0, &cx0);
-        sincospi(2.0 * y0, &sy0, &cy0);
+        sincospi(2.0 * (x0 - t), &sx0, &cx0);
+        sincospi(2.0 * (y0 - t), &sy0, &cy0);
+        sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
       }
 #pragma unroll 1
       for (int q = 0; q < NQ; ++q) {
@@ -331,8 +401,10 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
           double sz, cz, sw, cw;
           sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
           sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
-          forcing_mms(P, x, y, fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz),
-                      fma(sy0, cw, cy0 * sw), fma(cy0, cw, -sy0 * sw), st, ct, S, Fx, Fy);
+          const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
+          forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
+                      fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
+                      fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
         } else {
           forcing(P, x, y, t, st, ct, S, Fx, Fy);
         }
@@ -349,11 +421,6 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
         }
       }
     }
-  }
-  if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
-#pragma unroll 1
-    for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, s_tab + TB::L, c, u, hb, B11, B12, B21, B22, isd, r);
   }
   if (A.mode == 0) {
 #pragma unroll
@@ -411,55 +478,49 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Dirichlet ghost table: Gauss moments of the exact (xi, U, V, u, v) on each
-// boundary edge plus (H, |u.n|) at the lambda samples (solver.py:395-402,
-// 636-653; the pinv projection of :649-653 reduces to these moments).
+// Dirichlet ghost data: exact (xi, U, V, u, v) at the k+2 Gauss points of
+// every Dirichlet edge and (H, |u.n|) at the lambda samples (reference
+// solver.py:395-402, 636-653; the pinv(E) projection of :649-653 reduces to
+// the Gauss moments, taken in the stage kernel).  One thread per
+// (stage, slot, point); all stages of a step in one launch (the data depend
+// on time only).
 template <int k>
 __global__ void ghost_kernel(Tab T, Phys P, const int* __restrict__ bel,
-                             const int* __restrict__ bloc, int nb, double tv,
-                             const double* t_dev, double toff, double* ghost) {
+                             const int* __restrict__ bloc, int nb, int nstage, double t0,
+                             const double* t_dev, double3 toffs, double* ghost) {
   using O = Ord<k>;
-  constexpr int NT = O::NT;
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nb) return;
-  const double t = t_dev ? t_dev[0] + toff * t_dev[1] : tv;
+  using TB = Tabs<k>;
+  constexpr int NG = O::NG, NP = NG + 3;
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nstage * nb * NP) return;
+  const int pt = id % NP, slot = (id / NP) % nb, st = id / (NP * nb);
+  const double toff = st == 0 ? toffs.x : (st == 1 ? toffs.y : toffs.z);
+  const double t = t_dev ? t_dev[0] + toff * t_dev[1] : t0 + toff;
   const int64_t ld = T.ld;
-  const int e = bel[s], j = bloc[s];
+  const int e = bel[slot], j = bloc[slot];
   const double B11 = T.geo[e], B12 = T.geo[ld + e], B21 = T.geo[2 * ld + e], B22 = T.geo[3 * ld + e];
   const double a1x = T.geo[4 * ld + e], a1y = T.geo[5 * ld + e];
   // reference edge maps (x1, x2)(s): e0 (1-s, s), e1 (0, 1-s), e2 (s, 0)
   const double x0 = j == 0 ? 1.0 : 0.0, xs = j == 0 ? -1.0 : (j == 2 ? 1.0 : 0.0);
   const double y0 = j == 1 ? 1.0 : 0.0, ys = j == 0 ? 1.0 : (j == 1 ? -1.0 : 0.0);
-  const double dx = B11 * xs + B12 * ys, dy = B21 * xs + B22 * ys;
-  const double ln = sqrt(dx * dx + dy * dy), n1 = dy / ln, n2 = -dx / ln;
-  double mom[5 * NT];
-  O::gauss_moments(
-      [&](double sv, double* v) {
-        const double r1 = x0 + xs * sv, r2 = y0 + ys * sv;
-        const double x = a1x + B11 * r1 + B12 * r2, y = a1y + B21 * r1 + B22 * r2;
-        double xi, U, V;
-        exact3(P, x, y, t, xi, U, V);
-        const double H = hb_exact(P, x, y) + xi;
-        v[0] = xi;
-        v[1] = U;
-        v[2] = V;
-        v[3] = U / H;
-        v[4] = V / H;
-      },
-      mom);
-  double* out = ghost + (int64_t)s * (5 * NT + 6);
-#pragma unroll
-  for (int i = 0; i < 5 * NT; ++i) out[i] = mom[i];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const double sv = 0.5 * q;
-    const double r1 = x0 + xs * sv, r2 = y0 + ys * sv;
-    const double x = a1x + B11 * r1 + B12 * r2, y = a1y + B21 * r1 + B22 * r2;
-    double xi, U, V;
-    exact3(P, x, y, t, xi, U, V);
-    const double H = hb_exact(P, x, y) + xi;
-    out[5 * NT + q] = H;
-    out[5 * NT + 3 + q] = fabs((U * n1 + V * n2) / H);
+  const double sv = pt < NG ? TB::ptr()[TB::GS + pt] : 0.5 * (pt - NG);
+  const double r1 = x0 + xs * sv, r2 = y0 + ys * sv;
+  const double x = a1x + B11 * r1 + B12 * r2, y = a1y + B21 * r1 + B22 * r2;
+  double xi, U, V;
+  exact3(P, x, y, t, xi, U, V);
+  const double H = hb_exact(P, x, y) + xi;
+  double* out = ghost + ((int64_t)st * nb + slot) * (5 * NG + 6);
+  if (pt < NG) {
+    out[pt] = xi;
+    out[NG + pt] = U;
+    out[2 * NG + pt] = V;
+    out[3 * NG + pt] = U / H;
+    out[4 * NG + pt] = V / H;
+  } else {
+    const double dx = B11 * xs + B12 * ys, dy = B21 * xs + B22 * ys;
+    const double ln = sqrt(dx * dx + dy * dy);
+    out[5 * NG + pt - NG] = H;
+    out[5 * NG + 3 + pt - NG] = fabs((U * (dy / ln) - V * (dx / ln)) / H);
   }
 }
 
@@ -559,11 +620,14 @@ static void launch_velocity(qf_ctx* x, const double* c, double* u, int e0, int n
 }
 
 template <int k>
-static void launch_ghost(qf_ctx* x, double t, const double* t_dev, double toff, cudaStream_t s) {
+static void launch_ghost(qf_ctx* x, double t, const double* t_dev, int nstage, double3 toffs,
+                         cudaStream_t s) {
   const int nb = x->d.n_bnd;
   if (nb <= 0) return;
-  ghost_kernel<k><<<(nb + 127) / 128, 128, 0, s>>>(x->tab, x->phys, x->d.bnd_elem, x->d.bnd_local,
-                                                   nb, t, t_dev, toff, x->d.ghost);
+  const int n = nstage * nb * (Ord<k>::NG + 3);
+  ghost_kernel<k><<<(n + 127) / 128, 128, 0, s>>>(x->tab, x->phys, x->d.bnd_elem,
+                                                  x->d.bnd_local, nb, nstage, t, t_dev, toffs,
+                                                  x->d.ghost);
   g_launches++;
 }
 
@@ -584,7 +648,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
   x->d = *d;
   x->K = (d->order + 1) * (d->order + 2) / 2;
   x->NT = d->order + 1;
-  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->ld};
+  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->ld, d->n_bnd};
   x->phys.g = d->g;
   x->phys.fc = d->f_c;
   x->phys.tau = d->tau_bf;
@@ -621,7 +685,8 @@ int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, vo
 
 int qf_ghost(qf_ctx* x, double t, void* stream) {
   if (!x) return fail(QF_E_ARG, "null ctx");
-  QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 0.0, (cudaStream_t)stream);
+  QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 1, make_double3(0.0, 0.0, 0.0),
+              (cudaStream_t)stream);
   return cuda_check("ghost_kernel");
 }
 
@@ -629,7 +694,8 @@ int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms,
            double* lam, void* stream) {
   if (!x || !c || !u || !rhs) return fail(QF_E_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  if (terms & TERM_EDGE) QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 0.0, s);
+  if (terms & TERM_EDGE)
+    QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 1, make_double3(0.0, 0.0, 0.0), s);
   StageArgs a{};
   a.c = c;
   a.u = u;
@@ -687,10 +753,14 @@ static void step_impl(qf_ctx* x, double* c, double* u, double* work, double* t_d
   double* c2 = work + S;
   double* u2 = work + S + CU;
   const int k = x->d.order;
+  const int nst = k == 0 ? 1 : (k == 1 ? 2 : 3);
+  const double3 toffs = k == 1 ? make_double3(0.0, 1.0, 0.0) : make_double3(0.0, 1.0, 0.5);
+  QF_DISPATCH(k, launch_ghost, x, 0.0, t_dev, nst, toffs, s);
+  int gst = 0;
   auto stage = [&](const double* ci, const double* ui, const double* cb, double* co, double* uo,
                    double a, double b, double toff) {
-    QF_DISPATCH(k, launch_ghost, x, 0.0, t_dev, toff, s);
     StageArgs A{};
+    A.gstage = gst++;
     A.c = ci;
     A.u = ui;
     A.c0 = cb;
@@ -736,7 +806,7 @@ int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* 
 
 static int kernels_per_step(qf_ctx* x) {
   const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
-  return stages * (1 + (x->d.n_bnd > 0 ? 1 : 0)) + 1;
+  return stages + (x->d.n_bnd > 0 ? 1 : 0) + 1;
 }
 
 int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,

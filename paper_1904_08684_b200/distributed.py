@@ -1,0 +1,309 @@
+"""Multi-GPU: contiguous element blocks with a face-neighbour halo per stage.
+
+The grid shards naturally: each rank owns a block of elements
+(vertical strips of quad columns, or px x py rectangles on the unit-square
+meshes), stores copies of the neighbour-rank elements that share an edge
+with its own (the halo) after its owned elements, and after every RK stage
+sends the new (c, u) of its cut-adjacent elements to the ranks that hold
+them as halo.  No per-stage collective exists: lambda is per edge and dt is
+fixed; one allreduce(max) fixes a CFL dt and one allreduce(max) takes the
+step time.
+
+Overlap: owned elements are ordered interior-first; per stage the interior
+range runs on the compute stream while the previous stage's halo is still in
+flight, then the cut-adjacent range runs once the halo has arrived, and its
+result is gathered and exchanged on a communication stream while the next
+stage's interior range computes.
+
+The host logic (partitioning, halo lists, exchange) is shared by the GPU
+runner (NCCL over NVLink, ``qf_stage`` / ``qf_gather`` / ``qf_scatter``) and
+a CPU runner used by the ``gloo`` tests, whose stage executor is the
+test-only oracle (``oracle/trace_stage.py``).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .mesh import Mesh
+
+__all__ = ["strip_partition", "block_partition", "range_partition", "Halo", "build_halo",
+           "HaloExchange", "DistributedRunner", "bench_distributed"]
+
+
+# --------------------------------------------------------------- partitions
+def strip_partition(n: int, world: int) -> np.ndarray:
+    """Unit-square split mesh (build_unit_square_mesh(n)): strips of quad columns."""
+    q = np.arange(2 * n * n) // 2
+    col = q // n
+    return (col * world // n).astype(np.int64)
+
+
+def block_partition(n: int, px: int, py: int) -> np.ndarray:
+    """px x py rectangles of quads (C4: 4 x 2)."""
+    q = np.arange(2 * n * n) // 2
+    i, j = q // n, q % n
+    return ((i * px // n) * py + (j * py // n)).astype(np.int64)
+
+
+def range_partition(n_elem: int, world: int) -> np.ndarray:
+    """Generic meshes: contiguous element ranges of equal size."""
+    return (np.arange(n_elem) * world // max(n_elem, 1)).astype(np.int64)
+
+
+@dataclass
+class Halo:
+    """Local element order and exchange lists of one rank."""
+
+    rank: int
+    elements: np.ndarray          # global ids: owned (interior, then cut-adjacent), halo
+    n_own: int
+    n_int: int                    # owned elements without a remote neighbour
+    send: dict = field(default_factory=dict)   # peer -> local ids (owned), peer's halo order
+    recv: dict = field(default_factory=dict)   # peer -> local ids (halo)
+
+    @property
+    def n_local(self) -> int:
+        return len(self.elements)
+
+
+def build_halo(mesh: Mesh, part: np.ndarray, rank: int) -> Halo:
+    nbr = mesh.conn.nbr
+    own = np.flatnonzero(part == rank)
+    nb = nbr[own]
+    remote = (nb >= 0) & (part[np.maximum(nb, 0)] != rank)
+    cut = remote.any(axis=1)
+    own_order = np.concatenate([own[~cut], own[cut]])
+    n_own, n_int = len(own), int((~cut).sum())
+    rem = np.unique(nb[remote])
+    owner = part[rem]
+    order = np.lexsort((rem, owner))
+    halo = rem[order]
+    elements = np.concatenate([own_order, halo])
+    g2l = {int(g): i for i, g in enumerate(elements)}
+    recv, send = {}, {}
+    for p in np.unique(owner):
+        hp = halo[owner[order] == p]
+        recv[int(p)] = np.array([g2l[int(g)] for g in hp], dtype=np.int64)
+        # my owned elements adjacent to p, in global-id order (= p's halo order)
+        nbp = nbr[own_order]
+        mine = own_order[((nbp >= 0) & (part[np.maximum(nbp, 0)] == p)).any(axis=1)]
+        mine = np.sort(mine)
+        send[int(p)] = np.array([g2l[int(g)] for g in mine], dtype=np.int64)
+    return Halo(rank=rank, elements=elements, n_own=n_own, n_int=n_int, send=send, recv=recv)
+
+
+# ----------------------------------------------------------------- exchange
+class HaloExchange:
+    """Pack (c, u) rows of the send lists, P2P exchange, unpack into the halo.
+
+    ``c``/``u`` are [F][K][ld] tensors (device for NCCL, CPU for gloo).  On
+    the GPU, gather/scatter are the library kernels; the transfers are
+    ``torch.distributed.batch_isend_irecv`` (NCCL P2P over NVLink).
+    """
+
+    def __init__(self, halo: Halo, K: int, ld: int, device, lib=None):
+        import torch
+
+        self.torch = torch
+        self.halo, self.K, self.ld, self.lib = halo, K, ld, lib
+        self.rows = 5 * K
+        self.dev = device
+        self.peers = sorted(set(halo.send) | set(halo.recv))
+        self.sidx = {p: torch.as_tensor(halo.send.get(p, np.zeros(0, np.int64)).astype(np.int32),
+                                        device=device) for p in self.peers}
+        self.ridx = {p: torch.as_tensor(halo.recv.get(p, np.zeros(0, np.int64)).astype(np.int32),
+                                        device=device) for p in self.peers}
+        self.sbuf = {p: torch.empty(self.rows * len(self.sidx[p]), dtype=torch.float64,
+                                    device=device) for p in self.peers}
+        self.rbuf = {p: torch.empty(self.rows * len(self.ridx[p]), dtype=torch.float64,
+                                    device=device) for p in self.peers}
+
+    def _gather(self, c, u, p, stream):
+        n = len(self.sidx[p])
+        buf = self.sbuf[p]
+        if self.lib is not None:
+            s = stream.cuda_stream
+            self.lib.qf_gather(c.data_ptr(), self.ld, self.sidx[p].data_ptr(), n, 3 * self.K,
+                               buf.data_ptr(), s)
+            self.lib.qf_gather(u.data_ptr(), self.ld, self.sidx[p].data_ptr(), n, 2 * self.K,
+                               buf[3 * self.K * n:].data_ptr(), s)
+        else:
+            idx = self.sidx[p].long()
+            buf.view(self.rows, n)[: 3 * self.K] = c.view(3 * self.K, self.ld)[:, idx]
+            buf.view(self.rows, n)[3 * self.K:] = u.view(2 * self.K, self.ld)[:, idx]
+
+    def _scatter(self, c, u, p, stream):
+        n = len(self.ridx[p])
+        buf = self.rbuf[p]
+        if self.lib is not None:
+            s = stream.cuda_stream
+            self.lib.qf_scatter(buf.data_ptr(), self.ridx[p].data_ptr(), n, 3 * self.K,
+                                c.data_ptr(), self.ld, s)
+            self.lib.qf_scatter(buf[3 * self.K * n:].data_ptr(), self.ridx[p].data_ptr(), n,
+                                2 * self.K, u.data_ptr(), self.ld, s)
+        else:
+            idx = self.ridx[p].long()
+            c.view(3 * self.K, self.ld)[:, idx] = buf.view(self.rows, n)[: 3 * self.K]
+            u.view(2 * self.K, self.ld)[:, idx] = buf.view(self.rows, n)[3 * self.K:]
+
+    def exchange(self, c, u, stream=None):
+        """Blocking (w.r.t. ``stream``) halo update of (c, u)."""
+        import torch.distributed as dist
+
+        for p in self.peers:
+            self._gather(c, u, p, stream)
+        ops = []
+        for p in self.peers:
+            if len(self.sbuf[p]):
+                ops.append(dist.P2POp(dist.isend, self.sbuf[p], p))
+            if len(self.rbuf[p]):
+                ops.append(dist.P2POp(dist.irecv, self.rbuf[p], p))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for p in self.peers:
+            self._scatter(c, u, p, stream)
+
+
+def rk_plan(k: int):
+    """(src, dst, a, b, toff) per stage over buffers 0 (state), 1, 2."""
+    if k == 0:
+        return [(0, 1, 0.0, 1.0, 0.0)]
+    if k == 1:
+        return [(0, 1, 0.0, 1.0, 0.0), (1, 0, 0.5, 0.5, 1.0)]
+    return [(0, 1, 0.0, 1.0, 0.0), (1, 2, 0.75, 0.25, 1.0), (2, 0, 1.0 / 3.0, 2.0 / 3.0, 0.5)]
+
+
+# ------------------------------------------------------------- GPU runner
+class DistributedRunner:
+    """One rank of a partitioned run on the B200 path (one process per GPU)."""
+
+    def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int,
+                 world: int):
+        import torch
+        import torch.distributed as dist
+
+        from .solver import Discretization
+
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.k = rank, world, order
+        self.halo = build_halo(mesh, part, rank)
+        h = self.halo
+        self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own)
+        d = self.disc
+        self.K, self.ld = d.K, d.ld
+        self.lib = d._lib
+        self.ex = HaloExchange(h, d.K, d.ld, d.device, lib=self.lib)
+        c_all = d.project_fields()
+        self.c = d.upload_fields(c_all)
+        self.u = torch.zeros_like(self.c[:2])
+        self.c1, self.u1 = torch.zeros_like(self.c), torch.zeros_like(self.u)
+        self.c2, self.u2 = torch.zeros_like(self.c), torch.zeros_like(self.u)
+        s = torch.cuda.current_stream().cuda_stream
+        # halo velocities are element-local: solve them locally at start
+        d._check(self.lib.qf_velocity(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0,
+                                      h.n_local, s), "qf_velocity")
+        self.dt = d.dt
+        if scenario.cfl is not None:
+            lam = torch.zeros((3, self.ld), dtype=torch.float64, device=d.device)
+            out = torch.empty_like(self.c)
+            self.lib.qf_rhs(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0.0, 2, out.data_ptr(),
+                            lam.data_ptr(), s)
+            lmax = lam[:, : h.n_own].max().reshape(1)
+            hmin = torch.tensor([d.h_min], dtype=torch.float64, device=d.device)
+            dist.all_reduce(lmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(hmin, op=dist.ReduceOp.MIN)
+            self.dt = float(scenario.cfl) * float(hmin.item()) / float(lmax.item())
+        self.t = 0.0
+        self.comm = torch.cuda.Stream()
+        self.bufs = {0: (self.c, self.u), 1: (self.c1, self.u1), 2: (self.c2, self.u2)}
+
+    def step(self):
+        """One SSP-RK step: interior range overlapped with the halo exchange."""
+        torch = self.torch
+        d, lib, h = self.disc, self.lib, self.halo
+        main = torch.cuda.current_stream()
+        s = main.cuda_stream
+        plan = rk_plan(self.k)
+        for src, dst, a, b, toff in plan:
+            ts = self.t + toff * self.dt
+            if d.tables.bnd_elem.size:
+                lib.qf_ghost(d._ctx, ts, s)
+            ci, ui = self.bufs[src]
+            co, uo = self.bufs[dst]
+            c0 = self.c
+            # interior elements: no halo dependence
+            lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), c0.data_ptr(), co.data_ptr(),
+                         uo.data_ptr(), a, b, ts, self.dt, None, 0.0, 0, h.n_int, s)
+            main.wait_stream(self.comm)  # halo of `src` has arrived
+            lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), c0.data_ptr(), co.data_ptr(),
+                         uo.data_ptr(), a, b, ts, self.dt, None, 0.0, h.n_int,
+                         h.n_own - h.n_int, s)
+            self.comm.wait_stream(main)
+            with torch.cuda.stream(self.comm):
+                self.ex.exchange(co, uo, self.comm)
+        if self.k == 0:
+            self.c.copy_(self.c1)
+            self.u.copy_(self.u1)
+        self.t += self.dt
+
+    def sync(self):
+        self.torch.cuda.current_stream().wait_stream(self.comm)
+
+
+def bench_distributed(args, configs, metric):
+    """Weak scaling: N_rank = N_base^2 elements per GPU, strip partition."""
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from . import mesh as M
+    from . import scenario as S
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    k, n0, scen, dt, jit, desc = configs[args.config]
+    n0 = args.n or n0
+    n = int(round(n0 * math.sqrt(world)))
+    mesh = M.build_unit_square_mesh(n, jitter=jit, seed=7) if jit else M.build_unit_square_mesh(n)
+    scn = S.mms_scenario(dt=dt) if scen == "mms" else S.bump_scenario(seed=0, cfl=0.1)
+    part = strip_partition(n, world)
+    run = DistributedRunner(mesh, scn, k, part, rank, world)
+    for _ in range(args.warmup):
+        run.step()
+    run.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = run.lib.qf_launch_count()
+    e0.record()
+    for _ in range(args.steps):
+        run.step()
+    run.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    launches = run.lib.qf_launch_count() - n_launch0
+    dist.barrier()
+    ns = 1 if k == 0 else (2 if k == 1 else 3)
+    K = run.K
+    dof = 3 * K * mesh.n_triangles * ns * args.steps
+    t_ms = float(ms.item())
+    if rank == 0:
+        line = {"metric": metric, "value": dof / (t_ms * 1e-3), "unit": "DoF-updates/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc + f" weak-scaled to N={n}", "order": k, "n": n,
+                           "elements": mesh.n_triangles, "parallelism": f"strips x{world}",
+                           "l2": "not flushed (per-rank state > L2 at scale)"},
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

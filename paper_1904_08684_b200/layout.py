@@ -50,42 +50,62 @@ class ElementTables:
     h_min: float
 
 
-def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, n_alloc: int | None = None
+def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, elements=None, n_own=None
                  ) -> ElementTables:
-    """Geometry and neighbour codes for ``mesh`` (all elements owned)."""
+    """Geometry and neighbour codes.
+
+    ``elements`` (global ids, local order) restricts the tables to a
+    partition: the first ``n_own`` are updated by this context, the rest are
+    halo copies of neighbour-rank elements (geometry / bathymetry only, their
+    state arrives by exchange).  Every neighbour of an owned element must be
+    in ``elements``.
+    """
     geom, egeom = compute_geometry(mesh)
-    E = mesh.n_triangles
-    ld = pad_ld(n_alloc or E)
-    geo = np.zeros((6, ld))
-    geo[0, :E], geo[1, :E] = geom.B[:, 0, 0], geom.B[:, 0, 1]
-    geo[2, :E], geo[3, :E] = geom.B[:, 1, 0], geom.B[:, 1, 1]
-    geo[4, :E], geo[5, :E] = geom.a1[:, 0], geom.a1[:, 1]
     c = mesh.conn
+    if elements is None:
+        elements = np.arange(mesh.n_triangles)
+    elements = np.asarray(elements, dtype=np.int64)
+    n_loc = len(elements)
+    E = n_loc if n_own is None else int(n_own)
+    own = elements[:E]
+    ld = pad_ld(n_loc)
+    g2l = np.full(mesh.n_triangles, -1, dtype=np.int64)
+    g2l[elements] = np.arange(n_loc)
+    geo = np.zeros((6, ld))
+    B, a1 = geom.B[elements], geom.a1[elements]
+    geo[0, :n_loc], geo[1, :n_loc] = B[:, 0, 0], B[:, 0, 1]
+    geo[2, :n_loc], geo[3, :n_loc] = B[:, 1, 0], B[:, 1, 1]
+    geo[4, :n_loc], geo[5, :n_loc] = a1[:, 0], a1[:, 1]
+    nbr, nloc = c.nbr[own], c.nbr_local[own]
+    inner = nbr >= 0
+    lnb = np.where(inner, g2l[np.maximum(nbr, 0)], 0)
+    if (lnb[inner] < 0).any():
+        raise ValueError("partition is missing halo elements")
     code = np.zeros((3, ld), dtype=np.int64)
-    inner = c.nbr >= 0
-    code[:, :E] = np.where(inner, 4 * c.nbr + np.maximum(c.nbr_local, 0), 0).T
+    code[:, :E] = np.where(inner, 4 * lnb + np.maximum(nloc, 0), 0).T
     bel, bj = np.nonzero(~inner)
-    marks = -c.nbr_local[bel, bj]
+    marks = -nloc[bel, bj]
     dmask = np.isin(marks, list(dirichlet_markers))
     wmask = np.isin(marks, list(wall_markers))
     if not (dmask | wmask).all():
         bad = int(np.flatnonzero(~(dmask | wmask))[0])
-        raise ValueError(f"boundary edge of element {bel[bad]} has marker {marks[bad]}; "
+        raise ValueError(f"boundary edge of element {own[bel[bad]]} has marker {marks[bad]}; "
                          "only Dirichlet and wall markers are supported")
     # Dirichlet slots in mesh-edge order (reference pass_B order, solver.py:213-216)
-    eidx = c.elem_edge[bel, bj]
+    eidx = c.elem_edge[own[bel], bj]
     order = np.argsort(eidx, kind="stable")
     bel, bj, dmask = bel[order], bj[order], dmask[order]
     slot = np.cumsum(dmask) - 1
-    code[bj, bel] = np.where(dmask, -1 - (2 * slot + BND_DIRICHLET), -1 - (2 * 0 + BND_WALL))
+    code[bj, bel] = np.where(dmask, -1 - (2 * slot + BND_DIRICHLET), -1 - BND_WALL)
     if E and code.max() >= 2**31:
         raise ValueError("mesh too large for int32 neighbour codes")
-    # CFL height (solver.py:240-246)
-    lens = egeom.length[c.elem_edge]
-    h_min = float((geom.detB / lens.max(axis=1)).min()) if E else 0.0
+    # CFL height (solver.py:240-246) over the owned elements
+    lens = egeom.length[c.elem_edge[own]]
+    h_min = float((geom.detB[own] / lens.max(axis=1)).min()) if E else float("inf")
     return ElementTables(n_elem=E, ld=ld, geo=geo, nbr=code.astype(np.int32),
                          bnd_elem=bel[dmask].astype(np.int32),
-                         bnd_local=bj[dmask].astype(np.int32), detB=geom.detB, h_min=h_min)
+                         bnd_local=bj[dmask].astype(np.int32), detB=geom.detB[elements],
+                         h_min=h_min)
 
 
 def aos_to_soa(a: np.ndarray, ld: int) -> np.ndarray:

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _cabi
 from .layout import BND_DIRICHLET, build_tables, pad_ld
-from .mesh import Mesh, compute_geometry
+from .mesh import ElementGeometry, Mesh, compute_geometry
 from .scenario import KIND_NONE, Scenario
 from .symbolic import build_basis
 from .tensors import build_ref_tensors, triangle_rule
@@ -115,11 +115,14 @@ def _torch():
     return torch
 
 
-class Discretization:
-    """Mesh + order + scenario bound to device tables (reference solver.py:100-124)."""
+class HostSetup:
+    """Host-side (NumPy) setup shared by the device path and the CPU tests:
+    geometry, quadrature, P1 bathymetry, SoA tables (reference solver.py:103-270)."""
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
-                 device: int | None = None):
+                 elements=None, n_own: int | None = None):
+        """``elements``/``n_own`` restrict the discretization to a partition
+        (``distributed.py``): local order = owned elements then halo copies."""
         if backend not in ("einsum", "ir"):
             raise ValueError("backend must be 'einsum' or 'ir'")
         if scenario.hb_mode not in ("linear", "const"):
@@ -130,10 +133,22 @@ class Discretization:
         self.backend = backend  # accepted for signature compatibility only
         self.basis = build_basis(self.k)
         self.K = self.basis.size
-        self.geom, self.edge_geom = compute_geometry(mesh)
+        geom, self.edge_geom = compute_geometry(mesh)
+        self.partitioned = elements is not None
+        if elements is None:
+            self.elements = np.arange(mesh.n_triangles)
+            self.n_own = mesh.n_triangles
+            self.geom = geom
+        else:
+            self.elements = np.asarray(elements, dtype=np.int64)
+            self.n_own = len(self.elements) if n_own is None else int(n_own)
+            el = self.elements
+            self.geom = ElementGeometry(B=geom.B[el], detB=geom.detB[el],
+                                        sqrt_detB=geom.sqrt_detB[el], a1=geom.a1[el])
         self._setup_quadrature()
         self._setup_bathymetry()
-        self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers)
+        self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
+                                   self.elements if self.partitioned else None, self.n_own)
         self.h_min = self.tables.h_min
         needs_data = len(self.tables.bnd_elem) > 0 or scenario.forcing is not None \
             or scenario.mass_source is not None
@@ -147,7 +162,6 @@ class Discretization:
         self.phi_at_vertices = np.array(
             [[f.eval(*v) for v in ((0.0, 0.0), (1.0, 0.0), (0.0, 1.0))]
              for f in self.basis.functions])
-        self._setup_device(device)
 
     # ------------------------------------------------------------- setup
     @property
@@ -183,6 +197,38 @@ class Discretization:
         self.hb_mean = self.hb_coef[:, 0] / (math.sqrt(2.0) * sd)
         self._nh = keep
 
+    def project_fields(self) -> np.ndarray:
+        """Initial (xi, U, V) coefficients of every local element (owned + halo)."""
+        scn = self.scn
+        x, y = self.quad_xy[:, :, 0], self.quad_xy[:, :, 1]
+        if scn.initial is not None:
+            fields = scn.initial(x, y)
+        elif scn.exact is not None:
+            fields = scn.exact(x, y, 0.0)
+        else:
+            raise ValueError("scenario has no analytic solution to project")
+        sd = self.geom.sqrt_detB[:, None]
+        c = np.stack([sd * ((f * self.quad_w) @ self.quad_phi.T) for f in fields], axis=1)
+        H = (self.hb_coef + c[:, XI]) @ self.quad_phi / self.geom.sqrt_detB[:, None]
+        if (H < scn.h_min).any():
+            raise DryState(f"projected depth fell below h_min = {scn.h_min}")
+        return c
+
+    def hb_table(self) -> np.ndarray:
+        """[NH][ld] bathymetry rows of the SoA layout."""
+        hb = np.zeros((self._nh, self.tables.ld))
+        hb[:, : len(self.elements)] = self.hb_coef[:, : self._nh].T
+        return hb
+
+
+class Discretization(HostSetup):
+    """Mesh + order + scenario bound to device tables (reference solver.py:100-124)."""
+
+    def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
+                 device: int | None = None, elements=None, n_own: int | None = None):
+        super().__init__(mesh, scenario, order, backend, elements, n_own)
+        self._setup_device(device)
+
     def _setup_device(self, device):
         torch = _torch()
         self.torch = torch
@@ -193,14 +239,12 @@ class Discretization:
         self.ld = ld
         dev = self.device
         self._geo = torch.from_numpy(tb.geo).to(dev)
-        hb = np.zeros((self._nh, ld))
-        hb[:, :E] = self.hb_coef[:, : self._nh].T
-        self._hb = torch.from_numpy(hb).to(dev)
+        self._hb = torch.from_numpy(self.hb_table()).to(dev)
         self._nbr = torch.from_numpy(tb.nbr).to(dev)
         nb = len(tb.bnd_elem)
         self._bel = torch.from_numpy(tb.bnd_elem).to(dev)
         self._bloc = torch.from_numpy(tb.bnd_local).to(dev)
-        self._ghost = torch.zeros(max(nb, 1) * (5 * (self.k + 1) + 6), dtype=torch.float64,
+        self._ghost = torch.zeros(3 * max(nb, 1) * (5 * (self.k + 2) + 6), dtype=torch.float64,
                                   device=dev)
         scn = self.scn
         d = _cabi.QfDesc()
@@ -243,6 +287,16 @@ class Discretization:
     def _stream(self):
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
+    def upload_fields(self, arr: np.ndarray):
+        """(n, F, K) host array (n <= local elements) -> device SoA [F][K][ld]."""
+        t = self.torch
+        n, F, _ = arr.shape
+        a = t.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
+        out = t.zeros((F, self.K, self.ld), dtype=t.float64, device=self.device)
+        _cabi.check(self._lib.qf_pack(a.data_ptr(), out.data_ptr(), n, F, self.K, self.ld,
+                                      self._stream), "qf_pack")
+        return out
+
     def _empty_state(self):
         t = self.torch
         return (t.empty((3, self.K, self.ld), dtype=t.float64, device=self.device),
@@ -250,14 +304,14 @@ class Discretization:
 
     def _upload_c(self, c_host: np.ndarray):
         t = self.torch
-        E = self.tables.n_elem
+        E = len(c_host)
         a = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64))
         if self.device.type == "cuda":
             a = a.pin_memory()
         a = a.to(self.device, non_blocking=True)
         c, _ = self._empty_state()
         c.zero_()
-        _cabi.check(self._lib.qf_pack(a.data_ptr(), c.data_ptr(), E, 3, self.K, self.ld,
+        _cabi.check(self._lib.qf_pack(a.data_ptr(), c.data_ptr(), E, a.shape[1], self.K, self.ld,
                                       self._stream), "qf_pack")
         return c
 
@@ -317,22 +371,10 @@ class Discretization:
 
     def project_initial(self) -> State:
         """Project analytic (or non-analytic ``initial``) data at t = 0 (solver.py:288-303)."""
-        scn = self.scn
-        x, y = self.quad_xy[:, :, 0], self.quad_xy[:, :, 1]
-        if scn.initial is not None:
-            fields = scn.initial(x, y)
-        elif scn.exact is not None:
-            fields = scn.exact(x, y, 0.0)
-        else:
-            raise ValueError("scenario has no analytic solution to project")
-        sd = self.geom.sqrt_detB[:, None]
-        c = np.stack([sd * ((f * self.quad_w) @ self.quad_phi.T) for f in fields], axis=1)
-        H = (self.hb_coef + c[:, XI]) @ self.quad_phi / self.geom.sqrt_detB[:, None]
-        if (H < scn.h_min).any():
-            raise DryState(f"projected depth fell below h_min = {scn.h_min}")
+        c = self.project_fields()[: self.n_own]
         state = State(c=c, u=np.zeros((len(c), 2, self.K)), t=0.0)
         self.solve_velocity(state)
-        if not self._dt_fixed:
+        if not self._dt_fixed and not self.partitioned:
             self.dt = self.cfl_dt(state)
             self._dt_fixed = True
         return state
@@ -374,6 +416,8 @@ class Discretization:
 
     def compute_lambda(self, state: State, t: float) -> np.ndarray:
         """Per-edge LF speed in ``mesh.edges`` order (solver.py:340-406)."""
+        if self.partitioned:
+            raise NotImplementedError("compute_lambda on a partition: use lambda_local")
         _, lam = self._rhs_terms(state, t, _cabi.TERM_EDGE, want_lam=True)
         c = self.mesh.conn
         return lam[c.left_local, c.left]
