@@ -181,80 +181,149 @@ def rk_plan(k: int):
 
 
 # ------------------------------------------------------------- GPU runner
-class DistributedRunner:
-    """One rank of a partitioned run on the B200 path (one process per GPU)."""
+class PartitionRunner:
+    """Device state and stage launches of one partition (owned + halo)."""
+
+    def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int):
+        import torch
+
+        from .solver import Discretization
+
+        self.torch = torch
+        self.k = order
+        self.halo = build_halo(mesh, part, rank)
+        h = self.halo
+        self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own)
+        d = self.disc
+        self.K, self.ld, self.lib = d.K, d.ld, d._lib
+        self.c = d.upload_fields(d.project_fields())
+        self.u = torch.zeros_like(self.c[:2])
+        self.bufs = {0: (self.c, self.u),
+                     1: (torch.zeros_like(self.c), torch.zeros_like(self.u)),
+                     2: (torch.zeros_like(self.c), torch.zeros_like(self.u))}
+        s = torch.cuda.current_stream().cuda_stream
+        # halo velocities are element-local: solve them locally at start
+        d._check(self.lib.qf_velocity(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0,
+                                      h.n_local, s), "qf_velocity")
+        self.dt = d.dt
+        self.t = 0.0
+
+    def local_lambda_max(self) -> float:
+        d, torch = self.disc, self.torch
+        lam = torch.zeros((3, self.ld), dtype=torch.float64, device=d.device)
+        out = torch.empty_like(self.c)
+        d._check(self.lib.qf_rhs(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0.0, 2,
+                                 out.data_ptr(), lam.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream), "qf_rhs")
+        return float(lam[:, : self.halo.n_own].max().item())
+
+    def stage(self, si: int, part: str, stream):
+        """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range."""
+        src, dst, a, b, toff = rk_plan(self.k)[si]
+        d, lib, h = self.disc, self.lib, self.halo
+        s = stream.cuda_stream
+        ts = self.t + toff * self.dt
+        if part in ("interior", "all") and d.tables.bnd_elem.size:
+            lib.qf_ghost(d._ctx, ts, s)
+        ci, ui = self.bufs[src]
+        co, uo = self.bufs[dst]
+        e0, n = {"interior": (0, h.n_int), "boundary": (h.n_int, h.n_own - h.n_int),
+                 "all": (0, h.n_own)}[part]
+        if n > 0:
+            d._check(lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
+                                  co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None, 0.0, e0,
+                                  n, s), "qf_stage")
+        return co, uo
+
+    def end_step(self):
+        if self.k == 0:
+            self.c.copy_(self.bufs[1][0])
+            self.u.copy_(self.bufs[1][1])
+        self.t += self.dt
+
+
+class DistributedRunner(PartitionRunner):
+    """One rank of a partitioned run (one process per GPU, NCCL P2P halos)."""
 
     def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int,
                  world: int):
         import torch
         import torch.distributed as dist
 
-        from .solver import Discretization
-
-        self.torch, self.dist = torch, dist
-        self.rank, self.world, self.k = rank, world, order
-        self.halo = build_halo(mesh, part, rank)
-        h = self.halo
-        self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own)
-        d = self.disc
-        self.K, self.ld = d.K, d.ld
-        self.lib = d._lib
-        self.ex = HaloExchange(h, d.K, d.ld, d.device, lib=self.lib)
-        c_all = d.project_fields()
-        self.c = d.upload_fields(c_all)
-        self.u = torch.zeros_like(self.c[:2])
-        self.c1, self.u1 = torch.zeros_like(self.c), torch.zeros_like(self.u)
-        self.c2, self.u2 = torch.zeros_like(self.c), torch.zeros_like(self.u)
-        s = torch.cuda.current_stream().cuda_stream
-        # halo velocities are element-local: solve them locally at start
-        d._check(self.lib.qf_velocity(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0,
-                                      h.n_local, s), "qf_velocity")
-        self.dt = d.dt
+        super().__init__(mesh, scenario, order, part, rank)
+        self.dist, self.rank, self.world = dist, rank, world
+        self.ex = HaloExchange(self.halo, self.K, self.ld, self.disc.device, lib=self.lib)
         if scenario.cfl is not None:
-            lam = torch.zeros((3, self.ld), dtype=torch.float64, device=d.device)
-            out = torch.empty_like(self.c)
-            self.lib.qf_rhs(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0.0, 2, out.data_ptr(),
-                            lam.data_ptr(), s)
-            lmax = lam[:, : h.n_own].max().reshape(1)
-            hmin = torch.tensor([d.h_min], dtype=torch.float64, device=d.device)
+            lmax = torch.tensor([self.local_lambda_max()], dtype=torch.float64, device="cuda")
+            hmin = torch.tensor([self.disc.h_min], dtype=torch.float64, device="cuda")
             dist.all_reduce(lmax, op=dist.ReduceOp.MAX)
             dist.all_reduce(hmin, op=dist.ReduceOp.MIN)
             self.dt = float(scenario.cfl) * float(hmin.item()) / float(lmax.item())
-        self.t = 0.0
         self.comm = torch.cuda.Stream()
-        self.bufs = {0: (self.c, self.u), 1: (self.c1, self.u1), 2: (self.c2, self.u2)}
 
     def step(self):
         """One SSP-RK step: interior range overlapped with the halo exchange."""
         torch = self.torch
-        d, lib, h = self.disc, self.lib, self.halo
         main = torch.cuda.current_stream()
-        s = main.cuda_stream
-        plan = rk_plan(self.k)
-        for src, dst, a, b, toff in plan:
-            ts = self.t + toff * self.dt
-            if d.tables.bnd_elem.size:
-                lib.qf_ghost(d._ctx, ts, s)
-            ci, ui = self.bufs[src]
-            co, uo = self.bufs[dst]
-            c0 = self.c
-            # interior elements: no halo dependence
-            lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), c0.data_ptr(), co.data_ptr(),
-                         uo.data_ptr(), a, b, ts, self.dt, None, 0.0, 0, h.n_int, s)
-            main.wait_stream(self.comm)  # halo of `src` has arrived
-            lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), c0.data_ptr(), co.data_ptr(),
-                         uo.data_ptr(), a, b, ts, self.dt, None, 0.0, h.n_int,
-                         h.n_own - h.n_int, s)
+        for si in range(len(rk_plan(self.k))):
+            self.stage(si, "interior", main)          # needs no halo
+            main.wait_stream(self.comm)              # halo of the stage input arrived
+            co, uo = self.stage(si, "boundary", main)
             self.comm.wait_stream(main)
             with torch.cuda.stream(self.comm):
                 self.ex.exchange(co, uo, self.comm)
-        if self.k == 0:
-            self.c.copy_(self.c1)
-            self.u.copy_(self.u1)
-        self.t += self.dt
+        self.end_step()
 
     def sync(self):
         self.torch.cuda.current_stream().wait_stream(self.comm)
+
+
+class LocalMultiRunner:
+    """All partitions in one process on one GPU, halos moved by device
+    gather/scatter between the partitions' buffers (fake transport for
+    single-GPU tests of the partitioned kernels)."""
+
+    def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray):
+        import torch
+
+        self.torch = torch
+        world = int(part.max()) + 1
+        self.parts = [PartitionRunner(mesh, scenario, order, part, r) for r in range(world)]
+        self.k = order
+        idx = lambda a: torch.as_tensor(a.astype(np.int32), device="cuda")  # noqa: E731
+        self.links = []
+        for r, pr in enumerate(self.parts):
+            for p, recv in pr.halo.recv.items():
+                send = self.parts[p].halo.send[r]
+                self.links.append((r, p, idx(recv), idx(send)))
+
+    def step(self):
+        torch = self.torch
+        s = torch.cuda.current_stream()
+        for si in range(len(rk_plan(self.k))):
+            outs = [pr.stage(si, "all", s) for pr in self.parts]
+            for r, p, ridx, sidx in self.links:
+                dst, src = self.parts[r], self.parts[p]
+                n = len(ridx)
+                tmp = torch.empty(5 * dst.K * n, dtype=torch.float64, device="cuda")
+                for f, (arr_src, arr_dst, rows) in enumerate(
+                        ((outs[p][0], outs[r][0], 3 * dst.K), (outs[p][1], outs[r][1], 2 * dst.K))):
+                    off = 0 if f == 0 else 3 * dst.K * n
+                    src.lib.qf_gather(arr_src.data_ptr(), src.ld, sidx.data_ptr(), n, rows,
+                                      tmp[off:].data_ptr(), s.cuda_stream)
+                    dst.lib.qf_scatter(tmp[off:].data_ptr(), ridx.data_ptr(), n, rows,
+                                       arr_dst.data_ptr(), dst.ld, s.cuda_stream)
+        for pr in self.parts:
+            pr.end_step()
+
+    def owned_state(self):
+        """(global ids, c (n, 3, K)) per partition."""
+        out = []
+        for pr in self.parts:
+            n = pr.halo.n_own
+            c = pr.c[:, :, :n].permute(2, 0, 1).cpu().numpy()
+            out.append((pr.halo.elements[:n], c))
+        return out
 
 
 def bench_distributed(args, configs, metric):
