@@ -291,8 +291,15 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
   // of a 64-element tile, so on split-square meshes (element 2q lower, 2q+1
   // upper triangle of quad q) every warp is homogeneous in its local-edge
   // pairing and the neighbour trace switch never diverges.
+#ifndef QF_INTERLEAVE
+#define QF_INTERLEAVE 1
+#endif
+#if QF_INTERLEAVE
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int e = A.e0 + blockIdx.x * blockDim.x + (wid >> 1) * 64 + 2 * lane + (wid & 1);
+#else
+  const int e = A.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+#endif
   if (e >= A.e0 + A.n) return;
   const int64_t ld = T.ld;
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
