@@ -111,11 +111,12 @@ int qf_run(qf_ctx* ctx, int32_t n_steps, double* c, double* u, double* work, dou
            int32_t use_graph, void* stream);
 
 /* State <-> device layout: aos [E][F][K] (reference State.c / State.u)
- * <-> soa [F][K][ld]. */
+ * <-> soa [F][K][ld].  perm (optional, device int32 [n]): device slot d holds
+ * aos row perm[d] (locality order of the element tables); NULL = identity. */
 int qf_pack(const double* aos, double* soa, int32_t n_elem, int32_t F, int32_t K, int64_t ld,
-            void* stream);
+            const int32_t* perm, void* stream);
 int qf_unpack(const double* soa, double* aos, int32_t n_elem, int32_t F, int32_t K, int64_t ld,
-              void* stream);
+              const int32_t* perm, void* stream);
 
 /* gather / scatter rows for halo exchange: dst[r][i] = src[r][idx[i]] (rows
  * of length ld / n_idx) and the inverse scatter. */

@@ -57,8 +57,8 @@ def load(path: Path | None = None):
         "qf_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp]),
         "qf_step": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "qf_run": (C.c_int, [vp, i32, vp, vp, vp, vp, i32, vp]),
-        "qf_pack": (C.c_int, [vp, vp, i32, i32, i32, i64, vp]),
-        "qf_unpack": (C.c_int, [vp, vp, i32, i32, i32, i64, vp]),
+        "qf_pack": (C.c_int, [vp, vp, i32, i32, i32, i64, vp, vp]),
+        "qf_unpack": (C.c_int, [vp, vp, i32, i32, i32, i64, vp, vp]),
         "qf_gather": (C.c_int, [vp, i64, vp, i32, i32, vp, vp]),
         "qf_scatter": (C.c_int, [vp, vp, i32, i32, vp, i64, vp]),
         "qf_error": (C.c_int, [vp, C.POINTER(C.c_uint32), i32, vp]),

@@ -43,6 +43,12 @@ __device__ __forceinline__ double ldv(const double* p) {
   return v;
 }
 
+// detB with a fixed rounding sequence (no context-dependent FMA contraction),
+// so every thread that needs an element's detB gets the same bits
+__device__ __forceinline__ double det2(double b11, double b12, double b21, double b22) {
+  return __fma_rn(b11, b22, -__dmul_rn(b12, b21));
+}
+
 struct StageArgs {
   const double* __restrict__ c;   // [3][K][ld]
   const double* __restrict__ u;   // [2][K][ld]
@@ -88,16 +94,30 @@ __device__ __forceinline__ void trace_lit(int j, const double* f, double scale, 
   else
     O::trace2(f, t);
 #pragma unroll
-  for (int a = 0; a < O::NT; ++a) t[a] *= scale;
+  for (int a = 0; a < O::NT; ++a) t[a] = __dmul_rn(t[a], scale);
 }
 
+// threads (= elements) per block of the stage kernel
+template <int k>
+struct Blk {
+  static constexpr int value = k <= 2 ? 128 : 64;
+};
+
+// Shared-memory trace exchange.  Phase A: every thread writes its element's
+// physical trace moments (xi, U, V, u, v, h_b on local edges 0, 1, 2) to
+// s_tr[((j*6 + f)*NT + a)*BS + slot] and its mean depth term to s_hbm.
+// Phase B: a neighbour inside the block is read from there (no gather, no
+// recomputation); only neighbours outside the block are gathered from global
+// memory and traced.
 template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
-                                          int j, const double* __restrict__ sL, double B11,
+                                          int j, int slot, int blo, int bhi,
+                                          const double* __restrict__ s_tr,
+                                          const double* __restrict__ s_hbm, double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
-  constexpr int K = O::K, NT = O::NT, NH = O::NH;
+  constexpr int K = O::K, NT = O::NT, NH = O::NH, BS = Blk<k>::value;
   const int64_t ld = T.ld;
   // own outward normal: physical image of the reference edge direction
   const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
@@ -107,23 +127,11 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   const double n1 = dy * il, n2 = -dx * il;
 
   double own[6][NT], oth[6][NT];
-  double hbm_o;
-  {
-    double f[K];
 #pragma unroll
-    for (int fi = 0; fi < 6; ++fi) {
-      if (fi < 5) {
-        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+  for (int f = 0; f < 6; ++f)
 #pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = ldv(src + i * ld + e);
-      } else {
-#pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
-        hbm_o = f[0] * isd * 0.7071067811865476;
-      }
-      trace_lit<k>(j, f, isd, own[fi]);
-    }
-  }
+    for (int a = 0; a < NT; ++a) own[f][a] = s_tr[((j * 6 + f) * NT + a) * BS + slot];
+  const double hbm_o = s_hbm[slot];
   double hbm_n = hbm_o;
 
   const int code = T.nbr[j * ld + e];
@@ -131,33 +139,46 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   const double* gp = nullptr;
   if (code >= 0) {
     const int nb = code >> 2, jn = code & 3;
-    const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
-    const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
-    const double nisd = rsqrt(nB11 * nB22 - nB12 * nB21);
-    double f[K];
+    if (nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
+      const int ns = nb - blo;
 #pragma unroll
-    for (int fi = 0; fi < 6; ++fi) {
-      if (fi < 5) {
-        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+      for (int f = 0; f < 6; ++f)
 #pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
-      } else {
+        for (int a = 0; a < NT; ++a) {
+          const double v = s_tr[((jn * 6 + f) * NT + a) * BS + ns];
+          oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
+        }
+      hbm_n = s_hbm[ns];
+    } else {
+      const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
+      const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
+      const double nisd = rsqrt(det2(nB11, nB12, nB21, nB22));
+      double f[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
-        hbm_n = f[0] * nisd * 0.7071067811865476;
+      for (int fi = 0; fi < 6; ++fi) {
+        if (fi < 5) {
+          const double* src =
+              fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+          for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
+        } else {
+#pragma unroll
+          for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
+          hbm_n = __dmul_rn(__dmul_rn(f[0], nisd), 0.7071067811865476);
+        }
+        trace_lit<k>(jn, f, nisd, oth[fi]);
+#pragma unroll
+        for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
       }
-      trace_lit<k>(jn, f, nisd, oth[fi]);
-#pragma unroll
-      for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
     }
   } else {
-    const int v = -1 - code, slot = v >> 1;
+    const int v = -1 - code, bslot = v >> 1;
     if ((v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
       using TB = Tabs<k>;
       constexpr int NG = O::NG;
       dirichlet = true;
-      gp = T.ghost + ((int64_t)A.gstage * T.n_bnd + slot) * (5 * NG + 6);
-      const double* gw = sL - TB::L + TB::GPSI;
+      gp = T.ghost + ((int64_t)A.gstage * T.n_bnd + bslot) * (5 * NG + 6);
+      const double* gw = TB::ptr() + TB::GPSI;
 #pragma unroll
       for (int f = 0; f < 5; ++f) {
         double vals[NG];
@@ -273,40 +294,69 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
 template <int k>
 struct Occ {
 #ifndef QF_OCC2
-#define QF_OCC2 4
+#define QF_OCC2 3
 #endif
-  static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : (k == 3 ? 2 : 1));
+  static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : 4);
 };
 
 // ---------------------------------------------------------- stage kernel
+// dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 template <int k>
-__global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P, StageArgs A) {
+constexpr size_t stage_smem_bytes() {
+  return sizeof(double) * (Tabs<k>::SIZE + 3 * 6 * Ord<k>::NT * Blk<k>::value + Blk<k>::value);
+}
+
+template <int k>
+__global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
+    stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
   using TB = Tabs<k>;
-  constexpr int K = O::K, NH = O::NH, NQ = O::NQ;
-  __shared__ double s_tab[TB::SIZE];
-  for (int i = threadIdx.x; i < TB::SIZE; i += blockDim.x) s_tab[i] = TB::ptr()[i];
-  __syncthreads();
-  // interleaved mapping: warp 2w takes the even, warp 2w+1 the odd elements
-  // of a 64-element tile, so on split-square meshes (element 2q lower, 2q+1
-  // upper triangle of quad q) every warp is homogeneous in its local-edge
-  // pairing and the neighbour trace switch never diverges.
-#ifndef QF_INTERLEAVE
-#define QF_INTERLEAVE 1
-#endif
-#if QF_INTERLEAVE
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int e = A.e0 + blockIdx.x * blockDim.x + (wid >> 1) * 64 + 2 * lane + (wid & 1);
-#else
-  const int e = A.e0 + blockIdx.x * blockDim.x + threadIdx.x;
-#endif
-  if (e >= A.e0 + A.n) return;
+  constexpr int K = O::K, NH = O::NH, NQ = O::NQ, NT = O::NT, BS = Blk<k>::value;
+  extern __shared__ double smem[];
+  double* s_tab = smem;
+  double* s_tr = smem + TB::SIZE;
+  double* s_hbm = s_tr + 3 * 6 * NT * BS;
+  for (int i = threadIdx.x; i < TB::SIZE; i += BS) s_tab[i] = TB::ptr()[i];
+  const int slot = threadIdx.x;
+  const int blo = A.e0 + blockIdx.x * BS;
+  const int bhi = min(blo + BS, A.e0 + A.n);
+  const int e = blo + slot;
+  const bool active = e < bhi;
   const int64_t ld = T.ld;
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
-  const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
-  const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
-  const double det = B11 * B22 - B12 * B21, isd = rsqrt(det), sd = det * isd, idet = isd * isd;
+  const int ee = active ? e : blo;  // inactive threads read a valid element
+  const double B11 = ldg(T.geo + ee), B12 = ldg(T.geo + ld + ee);
+  const double B21 = ldg(T.geo + 2 * ld + ee), B22 = ldg(T.geo + 3 * ld + ee);
+  const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
+
+  if ((A.terms & TERM_EDGE) && active) {
+    // phase A: own trace moments on all three local edges -> shared memory
+    double f[K], t3[NT];
+#pragma unroll
+    for (int fi = 0; fi < 6; ++fi) {
+      if (fi < 5) {
+        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = ldv(src + i * ld + e);
+      } else {
+#pragma unroll
+        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
+        s_hbm[slot] = __dmul_rn(__dmul_rn(f[0], isd), 0.7071067811865476);
+      }
+      O::trace0(f, t3);
+#pragma unroll
+      for (int a = 0; a < NT; ++a) s_tr[((0 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      O::trace1(f, t3);
+#pragma unroll
+      for (int a = 0; a < NT; ++a) s_tr[((1 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      O::trace2(f, t3);
+#pragma unroll
+      for (int a = 0; a < NT; ++a) s_tr[((2 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+    }
+  }
+  __syncthreads();
+  if (!active) return;
 
   double r[3 * K];
 #pragma unroll
@@ -314,7 +364,7 @@ __global__ void __launch_bounds__(128, Occ<k>::value) stage_kernel(Tab T, Phys P
   if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
 #pragma unroll 1
     for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, s_tab + TB::L, B11, B12, B21, B22, isd, r);
+      edge_term<k>(T, P, A, e, j, slot, blo, bhi, s_tr, s_hbm, B11, B12, B21, B22, isd, r);
   }
   double c[3 * K], u[2 * K], hb[K];
 #pragma unroll
@@ -468,7 +518,7 @@ __global__ void __launch_bounds__(128)
   const int64_t ld = T.ld;
   const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
   const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
-  const double sd = sqrt(B11 * B22 - B12 * B21);
+  const double sd = sqrt(det2(B11, B12, B21, B22));
   double cc[3 * K], hb[K], uo[K], vo[K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
@@ -534,17 +584,19 @@ __global__ void ghost_kernel(Tab T, Phys P, const int* __restrict__ bel,
 __global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
 
 __global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
-                            int K, int64_t ld) {
+                            int K, int64_t ld, const int* __restrict__ perm) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
-  for (int i = 0; i < F * K; ++i) soa[i * ld + e] = aos[(int64_t)e * F * K + i];
+  const int64_t src = perm ? perm[e] : e;
+  for (int i = 0; i < F * K; ++i) soa[i * ld + e] = aos[src * F * K + i];
 }
 
 __global__ void unpack_kernel(const double* __restrict__ soa, double* __restrict__ aos, int n,
-                              int F, int K, int64_t ld) {
+                              int F, int K, int64_t ld, const int* __restrict__ perm) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
-  for (int i = 0; i < F * K; ++i) aos[(int64_t)e * F * K + i] = soa[i * ld + e];
+  const int64_t dst = perm ? perm[e] : e;
+  for (int i = 0; i < F * K; ++i) aos[dst * F * K + i] = soa[i * ld + e];
 }
 
 __global__ void gather_kernel(const double* __restrict__ src, int64_t ld, const int* __restrict__ idx,
@@ -611,10 +663,16 @@ static int cuda_check(const char* what) {
 
 template <int k>
 static void launch_stage(qf_ctx* x, const StageArgs& a, cudaStream_t s) {
-  const int bs = 128;
+  constexpr int bs = Blk<k>::value;
+  constexpr size_t smem = stage_smem_bytes<k>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stage_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
-  stage_kernel<k><<<grid, bs, 0, s>>>(x->tab, x->phys, a);
+  stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
   g_launches++;
 }
 
@@ -870,17 +928,17 @@ int qf_error(qf_ctx* x, uint32_t* bits, int32_t clear, void* stream) {
 }
 
 int qf_pack(const double* aos, double* soa, int32_t n, int32_t F, int32_t K, int64_t ld,
-            void* stream) {
+            const int32_t* perm, void* stream) {
   if (n <= 0) return QF_OK;
-  pack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(aos, soa, n, F, K, ld);
+  pack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(aos, soa, n, F, K, ld, perm);
   g_launches++;
   return cuda_check("pack_kernel");
 }
 
 int qf_unpack(const double* soa, double* aos, int32_t n, int32_t F, int32_t K, int64_t ld,
-              void* stream) {
+              const int32_t* perm, void* stream) {
   if (n <= 0) return QF_OK;
-  unpack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(soa, aos, n, F, K, ld);
+  unpack_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(soa, aos, n, F, K, ld, perm);
   g_launches++;
   return cuda_check("unpack_kernel");
 }

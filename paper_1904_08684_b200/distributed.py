@@ -78,7 +78,10 @@ def build_halo(mesh: Mesh, part: np.ndarray, rank: int) -> Halo:
     nb = nbr[own]
     remote = (nb >= 0) & (part[np.maximum(nb, 0)] != rank)
     cut = remote.any(axis=1)
-    own_order = np.concatenate([own[~cut], own[cut]])
+    from .mesh import locality_order
+
+    oi, ob = own[~cut], own[cut]
+    own_order = np.concatenate([oi[locality_order(mesh, oi)], ob[locality_order(mesh, ob)]])
     n_own, n_int = len(own), int((~cut).sum())
     rem = np.unique(nb[remote])
     owner = part[rem]

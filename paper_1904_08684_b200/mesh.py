@@ -47,6 +47,7 @@ __all__ = [
     "load_mesh",
     "save_mesh",
     "DIRICHLET",
+    "locality_order",
 ]
 
 DIRICHLET = 1
@@ -424,3 +425,30 @@ def load_mesh(path) -> Mesh:
             raise MeshParseError(f"line {no}: vertex index out of range")
         markers[(min(a, b), max(a, b))] = m
     return _finish(verts, tris, markers)
+
+
+def _spread16(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.uint64) & np.uint64(0xFFFF)
+    v = (v | (v << np.uint64(8))) & np.uint64(0x00FF00FF)
+    v = (v | (v << np.uint64(4))) & np.uint64(0x0F0F0F0F)
+    v = (v | (v << np.uint64(2))) & np.uint64(0x33333333)
+    v = (v | (v << np.uint64(1))) & np.uint64(0x55555555)
+    return v
+
+
+def locality_order(mesh: Mesh, elements=None) -> np.ndarray:
+    """Z-order (Morton) permutation of ``elements`` by centroid.
+
+    Consecutive runs of the result are compact patches of the mesh, so a
+    thread block of the stage kernel finds most neighbours of its elements
+    inside the block (shared-memory trace exchange instead of global
+    gathers).  Returns positions into ``elements`` (default: all).
+    """
+    el = np.arange(mesh.n_triangles) if elements is None else np.asarray(elements)
+    if len(el) == 0:
+        return np.zeros(0, dtype=np.int64)
+    cen = mesh.vertices[mesh.triangles[el]].mean(axis=1)
+    lo, hi = cen.min(axis=0), cen.max(axis=0)
+    q = ((cen - lo) / np.maximum(hi - lo, 1e-300) * 65535.0).astype(np.int64)
+    code = _spread16(q[:, 0]) | (_spread16(q[:, 1]) << np.uint64(1))
+    return np.argsort(code, kind="stable")

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _cabi
 from .layout import BND_DIRICHLET, build_tables, pad_ld
-from .mesh import ElementGeometry, Mesh, compute_geometry
+from .mesh import ElementGeometry, Mesh, compute_geometry, locality_order
 from .scenario import KIND_NONE, Scenario
 from .symbolic import build_basis
 from .tensors import build_ref_tensors, triangle_rule
@@ -147,8 +147,12 @@ class HostSetup:
                                         sqrt_detB=geom.sqrt_detB[el], a1=geom.a1[el])
         self._setup_quadrature()
         self._setup_bathymetry()
+        # device slot order: locality (Z-order) permutation of the local rows
+        # for a whole mesh; a partition's local order is already sorted
+        self.perm = None if self.partitioned else locality_order(mesh)
+        slots = self.elements if self.perm is None else self.elements[self.perm]
         self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
-                                   self.elements if self.partitioned else None, self.n_own)
+                                   slots, self.n_own)
         self.h_min = self.tables.h_min
         needs_data = len(self.tables.bnd_elem) > 0 or scenario.forcing is not None \
             or scenario.mass_source is not None
@@ -217,7 +221,8 @@ class HostSetup:
     def hb_table(self) -> np.ndarray:
         """[NH][ld] bathymetry rows of the SoA layout."""
         hb = np.zeros((self._nh, self.tables.ld))
-        hb[:, : len(self.elements)] = self.hb_coef[:, : self._nh].T
+        rows = self.hb_coef if self.perm is None else self.hb_coef[self.perm]
+        hb[:, : len(self.elements)] = rows[:, : self._nh].T
         return hb
 
 
@@ -242,6 +247,8 @@ class Discretization(HostSetup):
         self._hb = torch.from_numpy(self.hb_table()).to(dev)
         self._nbr = torch.from_numpy(tb.nbr).to(dev)
         nb = len(tb.bnd_elem)
+        self._perm = None if self.perm is None else \
+            torch.from_numpy(self.perm.astype(np.int32)).to(dev)
         self._bel = torch.from_numpy(tb.bnd_elem).to(dev)
         self._bloc = torch.from_numpy(tb.bnd_local).to(dev)
         self._ghost = torch.zeros(3 * max(nb, 1) * (5 * (self.k + 2) + 6), dtype=torch.float64,
@@ -287,6 +294,14 @@ class Discretization(HostSetup):
     def _stream(self):
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
+    def _perm_ptr(self, n: int):
+        """Device slot -> host row map for pack/unpack (None: identity)."""
+        if self._perm is None:
+            return None
+        if n != len(self._perm):
+            raise ValueError("permuted layout needs full-length host arrays")
+        return self._perm.data_ptr()
+
     def upload_fields(self, arr: np.ndarray):
         """(n, F, K) host array (n <= local elements) -> device SoA [F][K][ld]."""
         t = self.torch
@@ -294,7 +309,7 @@ class Discretization(HostSetup):
         a = t.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
         out = t.zeros((F, self.K, self.ld), dtype=t.float64, device=self.device)
         _cabi.check(self._lib.qf_pack(a.data_ptr(), out.data_ptr(), n, F, self.K, self.ld,
-                                      self._stream), "qf_pack")
+                                      self._perm_ptr(n), self._stream), "qf_pack")
         return out
 
     def _empty_state(self):
@@ -312,7 +327,7 @@ class Discretization(HostSetup):
         c, _ = self._empty_state()
         c.zero_()
         _cabi.check(self._lib.qf_pack(a.data_ptr(), c.data_ptr(), E, a.shape[1], self.K, self.ld,
-                                      self._stream), "qf_pack")
+                                      self._perm_ptr(E), self._stream), "qf_pack")
         return c
 
     def _download(self, ds: DeviceState):
@@ -321,10 +336,11 @@ class Discretization(HostSetup):
         ca = t.empty((E, 3, self.K), dtype=t.float64, device=self.device)
         ua = t.empty((E, 2, self.K), dtype=t.float64, device=self.device)
         s = self._stream
-        _cabi.check(self._lib.qf_unpack(ds.c.data_ptr(), ca.data_ptr(), E, 3, self.K, self.ld, s),
-                    "qf_unpack")
-        _cabi.check(self._lib.qf_unpack(ds.u.data_ptr(), ua.data_ptr(), E, 2, self.K, self.ld, s),
-                    "qf_unpack")
+        pp = self._perm_ptr(E)
+        _cabi.check(self._lib.qf_unpack(ds.c.data_ptr(), ca.data_ptr(), E, 3, self.K, self.ld, pp,
+                                        s), "qf_unpack")
+        _cabi.check(self._lib.qf_unpack(ds.u.data_ptr(), ua.data_ptr(), E, 2, self.K, self.ld, pp,
+                                        s), "qf_unpack")
         return ca.cpu().numpy(), ua.cpu().numpy()
 
     def _soa_to_host(self, x, F):
@@ -332,7 +348,7 @@ class Discretization(HostSetup):
         E = self.tables.n_elem
         a = t.empty((E, F, self.K), dtype=t.float64, device=self.device)
         _cabi.check(self._lib.qf_unpack(x.data_ptr(), a.data_ptr(), E, F, self.K, self.ld,
-                                        self._stream), "qf_unpack")
+                                        self._perm_ptr(E), self._stream), "qf_unpack")
         return a.cpu().numpy()
 
     def to_device(self, state: State, solve: bool = True) -> DeviceState:
@@ -401,7 +417,8 @@ class Discretization(HostSetup):
         uh = np.ascontiguousarray(state.u, dtype=np.float64)
         ua = self.torch.from_numpy(uh).to(self.device)
         self._check(self._lib.qf_pack(ua.data_ptr(), u.data_ptr(), self.tables.n_elem, 2, self.K,
-                                      self.ld, self._stream), "qf_pack")
+                                      self.ld, self._perm_ptr(self.tables.n_elem), self._stream),
+                    "qf_pack")
         out, _ = self._empty_state()
         lam = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device) \
             if want_lam else None
@@ -419,6 +436,10 @@ class Discretization(HostSetup):
         if self.partitioned:
             raise NotImplementedError("compute_lambda on a partition: use lambda_local")
         _, lam = self._rhs_terms(state, t, _cabi.TERM_EDGE, want_lam=True)
+        if self.perm is not None:
+            lam_rows = np.empty_like(lam)
+            lam_rows[:, self.perm] = lam
+            lam = lam_rows
         c = self.mesh.conn
         return lam[c.left_local, c.left]
 

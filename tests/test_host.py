@@ -237,3 +237,22 @@ def test_cabi_exports_every_header_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert lib.qf_abi_version() == 1
+
+
+def test_locality_order_is_a_compact_permutation():
+    m = M.build_unit_square_mesh(32)
+    p = M.locality_order(m)
+    assert np.array_equal(np.sort(p), np.arange(m.n_triangles))
+    # blocks of 128 consecutive slots: most neighbours stay inside the block
+    inv = np.empty_like(p)
+    inv[p] = np.arange(len(p))
+    nb = m.conn.nbr
+    inside = 0
+    total = 0
+    for b0 in range(0, len(p), 128):
+        el = p[b0:b0 + 128]
+        n = nb[el]
+        ok = n >= 0
+        total += ok.sum()
+        inside += ((inv[np.maximum(n, 0)] // 128 == b0 // 128) & ok).sum()
+    assert inside / total > 0.8
