@@ -111,7 +111,7 @@ struct Blk {
 // memory and traced.
 template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
-                                          int j, int slot, int blo, int bhi,
+                                          int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
                                           const double* __restrict__ s_hbm, double B11,
                                           double B12, double B21, double B22, double isd,
@@ -134,7 +134,6 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   const double hbm_o = s_hbm[slot];
   double hbm_n = hbm_o;
 
-  const int code = T.nbr[j * ld + e];
   bool dirichlet = false;
   const double* gp = nullptr;
   if (code >= 0) {
@@ -316,34 +315,42 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double* s_tab = smem;
   double* s_tr = smem + TB::SIZE;
   double* s_hbm = s_tr + 3 * 6 * NT * BS;
-  for (int i = threadIdx.x; i < TB::SIZE; i += BS) s_tab[i] = TB::ptr()[i];
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
   const int bhi = min(blo + BS, A.e0 + A.n);
   const int e = blo + slot;
   const bool active = e < bhi;
   const int64_t ld = T.ld;
-  const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
-  const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const int ee = active ? e : blo;  // inactive threads read a valid element
+  // issue every load of the element's own data up front: one memory round
+  // trip, overlapped with the table copy below
   const double B11 = ldg(T.geo + ee), B12 = ldg(T.geo + ld + ee);
   const double B21 = ldg(T.geo + 2 * ld + ee), B22 = ldg(T.geo + 3 * ld + ee);
+  const bool edges = (A.terms & TERM_EDGE) != 0;
+  int code[3] = {0, 0, 0};
+  double own_f[6 * K];
+  if (edges) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) code[j] = __ldg(T.nbr + j * ld + ee);
+#pragma unroll
+    for (int i = 0; i < 3 * K; ++i) own_f[i] = ldg(A.c + i * ld + ee);
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i) own_f[3 * K + i] = ldg(A.u + i * ld + ee);
+#pragma unroll
+    for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
+  }
+  for (int i = threadIdx.x; i < TB::SIZE; i += BS) s_tab[i] = TB::ptr()[i];
+  const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
+  const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
 
-  if ((A.terms & TERM_EDGE) && active) {
+  if (edges && active) {
     // phase A: own trace moments on all three local edges -> shared memory
-    double f[K], t3[NT];
+    double t3[NT];
+    s_hbm[slot] = __dmul_rn(__dmul_rn(own_f[5 * K], isd), 0.7071067811865476);
 #pragma unroll
     for (int fi = 0; fi < 6; ++fi) {
-      if (fi < 5) {
-        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
-#pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = ldv(src + i * ld + e);
-      } else {
-#pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
-        s_hbm[slot] = __dmul_rn(__dmul_rn(f[0], isd), 0.7071067811865476);
-      }
+      const double* f = own_f + fi * K;
       O::trace0(f, t3);
 #pragma unroll
       for (int a = 0; a < NT; ++a) s_tr[((0 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
@@ -361,18 +368,14 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double r[3 * K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
-  if (A.terms & TERM_EDGE) {  // reference solver.py:561-706
-#pragma unroll 1
-    for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, slot, blo, bhi, s_tr, s_hbm, B11, B12, B21, B22, isd, r);
-  }
+  // own data: still in registers from the prologue when edges are on
   double c[3 * K], u[2 * K], hb[K];
 #pragma unroll
-  for (int i = 0; i < 3 * K; ++i) c[i] = ldv(A.c + i * ld + e);
+  for (int i = 0; i < 3 * K; ++i) c[i] = edges ? own_f[i] : ldg(A.c + i * ld + e);
 #pragma unroll
-  for (int i = 0; i < 2 * K; ++i) u[i] = ldv(A.u + i * ld + e);
+  for (int i = 0; i < 2 * K; ++i) u[i] = edges ? own_f[3 * K + i] : ldg(A.u + i * ld + e);
 #pragma unroll
-  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
+  for (int i = 0; i < K; ++i) hb[i] = edges ? own_f[5 * K + i] : (i < NH ? ldg(T.hb + i * ld + e) : 0.0);
   const double* xi = c;
   const double* cU = c + K;
   const double* cV = c + 2 * K;
@@ -479,6 +482,12 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       }
     }
   }
+  if (edges) {  // reference solver.py:561-706
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j)
+      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_hbm, B11, B12, B21, B22, isd,
+                   r);
+  }
   if (A.mode == 0) {
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = r[i];
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   bool fin = true;
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) {
-    double v = c[i] + dt * r[i];
+    double v = ldv(A.c + i * ld + e) + dt * r[i];
     v = A.a != 0.0 ? fma(A.a, ldg(A.c0 + i * ld + e), A.b * v) : A.b * v;
     c[i] = v;
     fin = fin && isfinite(v);
