@@ -35,6 +35,12 @@
 
 namespace qf {
 
+#define QF_STR(x) #x
+#define QF_UNROLL(n) _Pragma(QF_STR(unroll n))
+#ifndef QF_QUNROLL
+#define QF_QUNROLL 1
+#endif
+
 // non-CSE'd read-only load: lets a phase re-read its element's data from L1
 // instead of keeping it live in registers across phases
 __device__ __forceinline__ double ldv(const double* p) {
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
         sincospi(2.0 * (y0 - t), &sy0, &cy0);
         sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
       }
-#pragma unroll 1
+      QF_UNROLL(QF_QUNROLL)
       for (int q = 0; q < NQ; ++q) {
         const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
         const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
