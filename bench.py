@@ -38,6 +38,9 @@ CONFIGS = {
     "c4": (2, 2048, "bumps", None, 0.2, "C4 jittered bumps+walls p=2 N=2048 SSP-RK3 CFL 0.1"),
     "c5": (4, 1448, "bumps", None, 0.0, "C5 weak bumps+walls p=4 N=1448/GPU SSP-RK3 CFL 0.1"),
 }
+# dram__bytes_read.sum + dram__bytes_write.sum of one stage_kernel launch
+# (stage 1 after the L2 flush) from `ncu --set full`, profiles/r01_*
+PROFILED_TRAFFIC = {"c2": 45.4e6}
 METRIC = "DG DoF-updates/s per RK stage (p=1..4) at 1/2/4/8 B200; % of HBM roofline"
 
 
@@ -187,15 +190,19 @@ def run_gpu(args):
     import torch
 
     from paper_1904_08684_b200 import _cabi
-    from paper_1904_08684_b200.solver import Discretization, State
+    from paper_1904_08684_b200.solver import Discretization
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1904_08684_b200 import distributed as QD
         return QD.bench_distributed(args, CONFIGS, METRIC)
     lib = _cabi.load()
@@ -209,70 +216,69 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
-    S5, S3 = 5 * K * ld, 3 * K * ld
-    c1, u1 = work[:S3], work[S3:S5]
-    c2, u2 = work[S5:S5 + S3], work[S5 + S3:]
-    coeffs = rk_coeffs(k)
-    bufs = {0: (ds.c, ds.u), 1: (c1, u1), 2: (c2, u2)}
-    plan = [(0, 1), (1, 2), (2, 0)] if k >= 2 else ([(0, 1), (1, 0)] if k == 1 else [(0, 1)])
+    ns = stages_of(k)
 
-    has_bnd = disc.tables.bnd_elem.size > 0
-    dt = disc.dt
-    tnow = [st0.t]
-
-    def one_step(evs=None):
-        t = tnow[0]
-        for si, ((src, dst), (a, b, toff)) in enumerate(zip(plan, coeffs)):
-            ts = t + toff * dt
-            if has_bnd:
-                _cabi.check(lib.qf_ghost(disc._ctx, ts, sp), "qf_ghost")
-            ci, ui = bufs[src]
-            co, uo = bufs[dst]
-            if evs is not None:
-                evs[si][0].record(stream)
-            _cabi.check(lib.qf_stage(disc._ctx, ci.data_ptr(), ui.data_ptr(), ds.c.data_ptr(),
-                                     co.data_ptr(), uo.data_ptr(), a, b, ts, dt, None, 0.0, 0,
-                                     -1, sp), "qf_stage")
-            if evs is not None:
-                evs[si][1].record(stream)
-        if k == 0:
-            ds.c.copy_(c1)
-            ds.u.copy_(u1)
-        tnow[0] = t + dt
+    def step():  # the library's SSP-RK step: 1 Dirichlet-data + ns stage launches + t advance
+        _cabi.check(lib.qf_step(disc._ctx, ds.c.data_ptr(), ds.u.data_ptr(), work.data_ptr(),
+                                ds.t_dev.data_ptr(), sp), "qf_step")
 
     for _ in range(args.warmup):
-        one_step()
+        step()
     torch.cuda.synchronize()
+    # ---- pass A (the reported value): whole steps, L2 flushed between steps
     clocks = Clocks(local)
     n0 = lib.qf_launch_count()
-    step_ms, stage_ms = [], []
+    step_ms = []
     for it in range(args.steps):
-        flush.fill_(float(it))  # L2 flush outside the timed events
+        flush.fill_(float(it))  # outside the timed events
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in plan]
         ev0.record(stream)
-        one_step(evs)
+        step()
         ev1.record(stream)
         clocks.sample()
         torch.cuda.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
-        stage_ms.append([a.elapsed_time(b) for a, b in evs])
     launches = lib.qf_launch_count() - n0
     clk = clocks.stop()
     disc._raise_errors("bench")
+    # ---- pass B (roofline): the same stages with an event pair around each
+    # stage_kernel launch (qf_stage), L2 flushed between steps as in pass A
+    S5, S3 = 5 * K * ld, 3 * K * ld
+    bufs = {0: (ds.c, ds.u), 1: (work[:S3], work[S3:S5]), 2: (work[S5:S5 + S3], work[S5 + S3:])}
+    plan = [(0, 1), (1, 2), (2, 0)] if k >= 2 else ([(0, 1), (1, 0)] if k == 1 else [(0, 1)])
+    has_bnd = disc.tables.bnd_elem.size > 0
+    stage_ms = []
+    tnow = float(ds.t_dev[0].item())
+    for it in range(min(args.steps, 50)):
+        flush.fill_(float(it))
+        evs = []
+        for (src, dst), (a, b, toff) in zip(plan, rk_coeffs(k)):
+            ts = tnow + toff * disc.dt
+            if has_bnd:
+                _cabi.check(lib.qf_ghost(disc._ctx, ts, sp), "qf_ghost")
+            (ci, ui), (co, uo) = bufs[src], bufs[dst]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _cabi.check(lib.qf_stage(disc._ctx, ci.data_ptr(), ui.data_ptr(), ds.c.data_ptr(),
+                                     co.data_ptr(), uo.data_ptr(), a, b, ts, disc.dt, None, 0.0,
+                                     0, -1, sp), "qf_stage")
+            e1.record(stream)
+            evs.append((e0, e1))
+        if k == 0:
+            ds.c.copy_(bufs[1][0])
+            ds.u.copy_(bufs[1][1])
+        tnow += disc.dt
+        torch.cuda.synchronize()
+        stage_ms.append([a.elapsed_time(b) for a, b in evs])
     total_ms = float(np.sum(step_ms))
-    ns = stages_of(k)
     dof = 3 * K * E * ns * args.steps
     value = dof / (total_ms * 1e-3)
-    # roofline of the dominant kernel (stage_kernel), algorithmic bytes
     peak, peak_src = peaks()
-    st = np.array(stage_ms)  # (steps, stages)
+    st = np.array(stage_ms)
     rvec = [0] + [1] * (ns - 1)
     bytes_step = sum(E * alg_bytes_per_elem(K, r) for r in rvec)
-    kern_ms = float(st.sum())
-    achieved = bytes_step * args.steps / (kern_ms * 1e-3) / 1e9
-    # e2e: public API with host states (H2D c, step, D2H c and u)
+    kern_ms_step = float(st.sum(axis=1).mean())
+    achieved = bytes_step / (kern_ms_step * 1e-3) / 1e9
     e2e = measure_e2e(disc, st0, max(3, min(args.steps, 20)))
     cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
     line = {
@@ -285,10 +291,10 @@ def run_gpu(args):
                    "dof_per_stage": 3 * K * E, "l2": "flushed (256 MB write) between timed steps",
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "stage_kernel", "kernel_ms_per_step": kern_ms / args.steps,
-                     "alg_bytes_per_step": bytes_step,
-                     "kernel_share_of_step": kern_ms / total_ms},
+                     "frac": achieved / peak, "traffic": PROFILED_TRAFFIC.get(args.config),
+                     "peak_source": peak_src, "kernel": "stage_kernel",
+                     "kernel_ms_per_step": kern_ms_step, "alg_bytes_per_step": bytes_step,
+                     "kernel_share_of_step": kern_ms_step / (total_ms / args.steps)},
         "hbm_roofline_dof_per_s": 3 * K * E * ns / (bytes_step / (peak * 1e9)),
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -332,6 +338,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override mesh resolution")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU runner even at world size 1 (smoke test)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
