@@ -162,6 +162,18 @@ def main():
     terms = stage_terms(disc, st0, 0.0)
     st = disc.step(disc.step(st0))
     np.savez_compressed(HERE / "ring_k1.npz", c0=st0.c, c2=st.c, **terms)
+    # G. MMS convergence sweeps (reference errors for the EOC tests)
+    for k, ns, dt, steps in ((1, (8, 16, 32), 1e-4, 200), (2, (8, 16), 2e-5, 200),
+                             (3, (4, 8), 2e-5, 100)):
+        errs = []
+        for n in ns:
+            m = unit_square(R, n)
+            scn = mms_scenario(R, dt=dt, t_end=steps * dt)
+            disc = Disc(m, scn, k)
+            st = disc.run()
+            errs.append(R.harness.l2_error(disc, st, st.t).errors())
+        np.savez_compressed(HERE / f"sweep_p{k}.npz", n=np.array(ns), err=np.array(errs),
+                            dt=dt, steps=steps)
     print("golden fixtures written to", HERE)
 
 

@@ -148,3 +148,33 @@ def test_partitioned_gpu_equals_single_domain(k, case, part):
     for ids, c in run.owned_state():
         got[ids] = c
     assert np.array_equal(got, out.c)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_mms_convergence_matches_reference(golden, k):
+    """BASELINE MMS sweep: GPU L2 errors and EOCs equal the reference's
+    (harness.l2_error on reference runs, tests/golden/sweep_p{k}.npz)."""
+    from paper_1904_08684_b200 import harness as Hn, mesh as M, scenario as S
+    g = golden(f"sweep_p{k}.npz")
+    dt, steps = float(g["dt"]), int(g["steps"])
+    scn = S.mms_scenario(dt=dt, t_end=steps * dt)
+    tab = Hn.convergence_study(k, list(g["n"]), scenario=scn,
+                               mesh_builder=lambda n: M.build_unit_square_mesh(int(n)))
+    got = np.array([r.errors() for r in tab.rows])
+    assert np.allclose(got, g["err"], rtol=1e-9, atol=0)
+    ref_eoc = np.log2(g["err"][:-1] / g["err"][1:])
+    assert np.allclose(np.array(tab.eoc()), ref_eoc, atol=1e-8)
+
+
+@pytest.mark.slow
+def test_c2_convergence_sweep_gpu():
+    """BASELINE C2 sweep N = 16..256, p = 2, SSP-RK3, dt = 2e-5, 1000 steps:
+    EOC(xi) ~ 3 (reference measured 2.94 / 2.99 for 16->32->64)."""
+    from paper_1904_08684_b200 import harness as Hn, mesh as M, scenario as S
+    scn = S.mms_scenario(dt=2e-5, t_end=1000 * 2e-5)
+    tab = Hn.convergence_study(2, [16, 32, 64, 128, 256], scenario=scn,
+                               mesh_builder=lambda n: M.build_unit_square_mesh(int(n)))
+    eoc = np.array(tab.eoc())
+    print(tab.to_csv())
+    assert (eoc[:, 0] > 2.7).all() and (eoc[:, 0] < 3.3).all()
+    assert (eoc[:3, 1:] > 2.6).all()
