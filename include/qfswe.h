@@ -83,6 +83,13 @@ void qf_destroy(qf_ctx* ctx);
  * [e0, e0+n) of state c (n < 0: all owned elements). */
 int qf_velocity(qf_ctx* ctx, const double* c, double* u, int32_t e0, int32_t n, void* stream);
 
+/* Device-side setup (project_initial / P1 bathymetry, solver.py:139-168,
+ * 282-303): project the field program `prog` (see qf_kernels.cu) onto the
+ * basis for the first n element slots: c[3][K][ld] and hb[NH][ld]; latches
+ * QF_BIT_DRY if the projected depth falls below h_min at a quadrature point. */
+int qf_project(qf_ctx* ctx, const double* prog, int32_t n, double h_min, double* c, double* hb,
+               void* stream);
+
 /* Dirichlet ghost data at time t into stage table 0 (solver.py:395-402, 636-653);
  * qf_stage reads table 0, qf_step/qf_run fill all stage tables themselves. */
 int qf_ghost(qf_ctx* ctx, double t, void* stream);

@@ -17,7 +17,7 @@ BIT_DRY, BIT_SINGULAR, BIT_NONFINITE = 1, 2, 4
 TERM_VOLUME, TERM_EDGE, TERM_SOURCE, TERM_ALL = 1, 2, 4, 7
 
 EXPORTS = (
-    "qf_create", "qf_destroy", "qf_velocity", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
+    "qf_create", "qf_destroy", "qf_velocity", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
     "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill",
     "qf_launch_count", "qf_last_error", "qf_abi_version",
 )
@@ -53,6 +53,7 @@ def load(path: Path | None = None):
         "qf_destroy": (None, [vp]),
         "qf_velocity": (C.c_int, [vp, vp, vp, i32, i32, vp]),
         "qf_ghost": (C.c_int, [vp, d, vp]),
+        "qf_project": (C.c_int, [vp, vp, i32, d, vp, vp, vp]),
         "qf_rhs": (C.c_int, [vp, vp, vp, d, i32, vp, vp, vp]),
         "qf_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp]),
         "qf_step": (C.c_int, [vp, vp, vp, vp, vp, vp]),

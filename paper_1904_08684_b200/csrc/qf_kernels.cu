@@ -37,6 +37,15 @@ namespace qf {
 
 #define QF_STR(x) #x
 #define QF_UNROLL(n) _Pragma(QF_STR(unroll n))
+#ifndef QF_EN_VOL
+#define QF_EN_VOL 1
+#endif
+#ifndef QF_EN_SRC
+#define QF_EN_SRC 1
+#endif
+#ifndef QF_EN_EDGE
+#define QF_EN_EDGE 1
+#endif
 #ifndef QF_QUNROLL
 #define QF_QUNROLL 1
 #endif
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double* cU = c + K;
   const double* cV = c + 2 * K;
 
-  if (A.terms & TERM_VOL) {  // Eqs. (15)-(16), reference solver.py:410-485
+  if (QF_EN_VOL && (A.terms & TERM_VOL)) {  // Eqs. (15)-(16), reference solver.py:410-485
     double al[K], be[K], ra[K], rb[K], wv[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       }
     }
   }
-  if (A.terms & TERM_SRC) {  // reference solver.py:708-725 (+ xi mass source)
+  if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725 (+ xi mass source)
     double d1, d2;
     O::hb_dref(hb, d1, d2);
     const double i32 = idet * isd;
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       }
     }
   }
-  if (edges) {  // reference solver.py:561-706
+  if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
 #pragma unroll 1
     for (int j = 0; j < 3; ++j)
       edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_hbm, B11, B12, B21, B22, isd,
@@ -596,6 +605,86 @@ __global__ void ghost_kernel(Tab T, Phys P, const int* __restrict__ bel,
   }
 }
 
+// Device-side setup: L2 projection of the initial state
+// and of the bathymetry onto the normalised basis at the reference's
+// degree-(2k+2) collapsed Gauss points (solver.py:139-168, 282-303), for
+// meshes too large for the host NumPy path.  Field program `prog`:
+//   [0] hb kind (0: bilinear from Phys.p, 1: base + amp * sum sin(k.x + phi))
+//   [1] init kind (0: scenario exact data at t = 0, 1: Gaussian bumps at rest)
+//   [2] n_modes  [3] n_bumps  [4] base  [5] amp
+//   then n_modes x (kx, ky, phi), then n_bumps x (A, sigma, cx, cy)
+// After projecting, the projected depth is checked at the quadrature points
+// (DryState if H < h_min, solver.py:305-311).
+template <int k>
+__global__ void project_kernel(Tab T, Phys P, const double* __restrict__ prog, int n,
+                               double h_min, double* __restrict__ c, double* __restrict__ hb_out,
+                               unsigned* err) {
+  using O = Ord<k>;
+  using TB = Tabs<k>;
+  constexpr int K = O::K, NH = O::NH, NQ = O::NQ;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int64_t ld = T.ld;
+  const double B11 = T.geo[e], B12 = T.geo[ld + e], B21 = T.geo[2 * ld + e], B22 = T.geo[3 * ld + e];
+  const double a1x = T.geo[4 * ld + e], a1y = T.geo[5 * ld + e];
+  const double sd = sqrt(det2(B11, B12, B21, B22));
+  const int hk = (int)prog[0], ik = (int)prog[1], nm = (int)prog[2], nbmp = (int)prog[3];
+  const double* modes = prog + 6;
+  const double* bumps = modes + 3 * nm;
+  double acc[4][K];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int p = 0; p < K; ++p) acc[f][p] = 0.0;
+  const double* tab = TB::ptr();
+  for (int q = 0; q < NQ; ++q) {
+    const double x1 = tab[TB::QX + q], x2 = tab[TB::QY + q];
+    const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+    double hbv;
+    if (hk == 1) {
+      double s = 0.0;
+      for (int m = 0; m < nm; ++m) s += sin(modes[3 * m] * x + modes[3 * m + 1] * y + modes[3 * m + 2]);
+      hbv = prog[4] + prog[5] * s;
+    } else {
+      hbv = hb_exact(P, x, y);
+    }
+    double xi = 0.0, U = 0.0, V = 0.0;
+    if (ik == 1) {
+      for (int b = 0; b < nbmp; ++b) {
+        const double dx = x - bumps[4 * b + 2], dy = y - bumps[4 * b + 3], s = bumps[4 * b + 1];
+        xi += bumps[4 * b] * exp(-(dx * dx + dy * dy) / (2.0 * s * s));
+      }
+    } else {
+      exact3(P, x, y, 0.0, xi, U, V);
+    }
+    const double v[4] = {xi, U, V, hbv};
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const double w = tab[TB::P + q * K + p];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) acc[f][p] = fma(w, v[f], acc[f][p]);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int p = 0; p < K; ++p) c[(f * K + p) * ld + e] = sd * acc[f][p];
+#pragma unroll
+  for (int p = 0; p < NH; ++p) hb_out[p * ld + e] = sd * acc[3][p];
+  // projected depth at the quadrature points (P1 bathymetry + xi)
+  bool dry = false;
+  for (int q = 0; q < NQ; ++q) {
+    double H = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const double hbp = p < NH ? sd * acc[3][p] : 0.0;
+      H = fma(hbp + sd * acc[0][p], tab[TB::PHI + q * K + p], H);
+    }
+    dry = dry || !(H / sd >= h_min);
+  }
+  if (dry) atomicOr(err, BIT_DRY);
+}
+
 __global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
 
 __global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
@@ -651,6 +740,7 @@ struct qf_ctx {
   cudaGraphExec_t graph = nullptr;
   const void* gkey[4] = {nullptr, nullptr, nullptr, nullptr};
   int graph_launches = 0;
+  cudaStream_t stream_hint = nullptr;
 };
 
 static thread_local std::string g_last_error;
@@ -711,6 +801,15 @@ static void launch_ghost(qf_ctx* x, double t, const double* t_dev, int nstage, d
   g_launches++;
 }
 
+template <int k>
+static void launch_project(qf_ctx* x, const double* prog, int n, double h_min, double* c,
+                           double* hb) {
+  if (n <= 0) return;
+  project_kernel<k><<<(n + 127) / 128, 128, 0, x->stream_hint>>>(x->tab, x->phys, prog, n, h_min,
+                                                                  c, hb, x->err);
+  g_launches++;
+}
+
 extern "C" {
 
 int qf_abi_version(void) { return 1; }
@@ -761,6 +860,14 @@ int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, vo
   }
   QF_DISPATCH(x->d.order, launch_velocity, x, c, u, e0, n, (cudaStream_t)stream);
   return cuda_check("velocity_kernel");
+}
+
+int qf_project(qf_ctx* x, const double* prog, int32_t n, double h_min, double* c, double* hb,
+               void* stream) {
+  if (!x || !prog || !c || !hb) return fail(QF_E_ARG, "null argument");
+  x->stream_hint = (cudaStream_t)stream;
+  QF_DISPATCH(x->d.order, launch_project, x, prog, n, h_min, c, hb);
+  return cuda_check("project_kernel");
 }
 
 int qf_ghost(qf_ctx* x, double t, void* stream) {

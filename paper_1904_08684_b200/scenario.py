@@ -102,6 +102,20 @@ class Scenario:
     cfl: float | None = None                 # dt = cfl * h_min / lambda_max(t=0)
     device: DeviceScenario = field(default_factory=DeviceScenario)
 
+    bump_params: dict | None = None          # drawn bump/mode parameters (bump_scenario)
+
+    def field_program(self) -> np.ndarray | None:
+        """Device field program for qf_project (csrc/qf_kernels.cu), or None."""
+        if self.bump_params is not None:
+            bp = self.bump_params
+            modes = np.column_stack([bp["kv"], bp["ph"]]).ravel()
+            bumps = np.column_stack([bp["A"], bp["sig"], bp["cen"]]).ravel()
+            head = [1.0, 1.0, len(bp["ph"]), len(bp["A"]), 1.0, 0.2]
+            return np.concatenate([head, modes, bumps]).astype(np.float64)
+        if self.device.kind != KIND_NONE and self.initial is None:
+            return np.zeros(6)
+        return None
+
     def exact_with_velocity(self, x, y, t):
         """Analytic (xi, U, V, u, v); u = U/H with H = hb + xi."""
         xi, U, V = self.exact(x, y, t)
@@ -299,6 +313,7 @@ def bump_fields(seed: int = 0, n_bumps: int = 16, n_modes: int = 8,
                     r2 = (x - cen[j, 0]) ** 2 + (y - cen[j, 1]) ** 2
                     acc = acc + A[j] * np.exp(-r2 / (2.0 * sig[j] ** 2))
                 return acc
+            xi0.params = dict(A=A, sig=sig, cen=cen, kv=kv, ph=ph)
             return xi0, hb, s
     raise ValueError("no admissible bathymetry seed found")
 
@@ -316,6 +331,7 @@ def bump_scenario(seed: int = 0, cfl: float = 0.1, **kw) -> Scenario:
         return v, np.zeros_like(v), np.zeros_like(v)
 
     scn.initial = initial
+    scn.bump_params = xi0.params
     scn.device = DeviceScenario(KIND_NONE)
     return scn
 

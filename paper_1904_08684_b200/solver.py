@@ -119,10 +119,15 @@ class HostSetup:
     """Host-side (NumPy) setup shared by the device path and the CPU tests:
     geometry, quadrature, P1 bathymetry, SoA tables (reference solver.py:103-270)."""
 
+    #: local element count from which setup projections run on the device
+    DEVICE_SETUP_MIN = 1_000_000
+
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
-                 elements=None, n_own: int | None = None):
+                 elements=None, n_own: int | None = None, device_setup: bool | None = None):
         """``elements``/``n_own`` restrict the discretization to a partition
-        (``distributed.py``): local order = owned elements then halo copies."""
+        (``distributed.py``): local order = owned elements then halo copies.
+        ``device_setup`` moves the initial / bathymetry projections to the GPU
+        (``qf_project``; default: automatic for large meshes)."""
         if backend not in ("einsum", "ir"):
             raise ValueError("backend must be 'einsum' or 'ir'")
         if scenario.hb_mode not in ("linear", "const"):
@@ -145,8 +150,16 @@ class HostSetup:
             el = self.elements
             self.geom = ElementGeometry(B=geom.B[el], detB=geom.detB[el],
                                         sqrt_detB=geom.sqrt_detB[el], a1=geom.a1[el])
+        prog = scenario.field_program()
+        if device_setup is None:
+            device_setup = prog is not None and len(self.elements) >= self.DEVICE_SETUP_MIN
+        if device_setup and prog is None:
+            raise ValueError(f"scenario {scenario.name!r} has no device field program")
+        self.device_setup = bool(device_setup)
+        self._nh = 1 if self.k == 0 else 3
         self._setup_quadrature()
-        self._setup_bathymetry()
+        if not self.device_setup:
+            self._setup_bathymetry()
         # device slot order: locality (Z-order) permutation of the local rows
         # for a whole mesh; a partition's local order is already sorted
         self.perm = None if self.partitioned else locality_order(mesh)
@@ -177,8 +190,15 @@ class HostSetup:
         pts, wts = triangle_rule(2 * self.k + 2)
         self.quad_ref, self.quad_w = pts, wts
         self.quad_phi = np.array([f.eval(pts[:, 0], pts[:, 1]) for f in self.basis.functions])
-        B, a1 = self.geom.B, self.geom.a1
-        self.quad_xy = np.einsum("eab,qb->eqa", B, pts) + a1[:, None, :]
+        self._quad_xy = None
+
+    @property
+    def quad_xy(self) -> np.ndarray:
+        """(E, Q, 2) physical quadrature points (built on first use)."""
+        if self._quad_xy is None:
+            B, a1 = self.geom.B, self.geom.a1
+            self._quad_xy = np.einsum("eab,qb->eqa", B, self.quad_ref) + a1[:, None, :]
+        return self._quad_xy
 
     def _setup_bathymetry(self):
         """P1 projection of h_b and its constant gradient (solver.py:139-168)."""
@@ -199,7 +219,6 @@ class HostSetup:
         else:
             self.hb_grad = np.zeros((len(sd), 2))
         self.hb_mean = self.hb_coef[:, 0] / (math.sqrt(2.0) * sd)
-        self._nh = keep
 
     def project_fields(self) -> np.ndarray:
         """Initial (xi, U, V) coefficients of every local element (owned + halo)."""
@@ -219,7 +238,7 @@ class HostSetup:
         return c
 
     def hb_table(self) -> np.ndarray:
-        """[NH][ld] bathymetry rows of the SoA layout."""
+        """[NH][ld] bathymetry rows of the SoA layout (host setup path)."""
         hb = np.zeros((self._nh, self.tables.ld))
         rows = self.hb_coef if self.perm is None else self.hb_coef[self.perm]
         hb[:, : len(self.elements)] = rows[:, : self._nh].T
@@ -244,7 +263,10 @@ class Discretization(HostSetup):
         self.ld = ld
         dev = self.device
         self._geo = torch.from_numpy(tb.geo).to(dev)
-        self._hb = torch.from_numpy(self.hb_table()).to(dev)
+        if self.device_setup:
+            self._hb = torch.zeros((self._nh, ld), dtype=torch.float64, device=dev)
+        else:
+            self._hb = torch.from_numpy(self.hb_table()).to(dev)
         self._nbr = torch.from_numpy(tb.nbr).to(dev)
         nb = len(tb.bnd_elem)
         self._perm = None if self.perm is None else \
@@ -273,6 +295,15 @@ class Discretization(HostSetup):
         self._ctx = ctx
         self._lib = lib
         self._work = None
+        if self.device_setup:
+            self._prog = torch.from_numpy(self.scn.field_program()).to(dev)
+            c0, _ = self._empty_state()
+            c0.zero_()
+            self._check(lib.qf_project(ctx, self._prog.data_ptr(), len(self.elements),
+                                       float(self.scn.h_min), c0.data_ptr(), self._hb.data_ptr(),
+                                       self._stream), "qf_project")
+            self._c_init = c0
+            self._raise_errors("initial projection")
 
     def _max_quad_angle(self) -> float:
         """max |2 pi (x_q - x_centroid)| over quadrature points (MMS Taylor gate)."""
@@ -385,8 +416,34 @@ class Discretization(HostSetup):
         vals = fn(x, y) if t is None else fn(x, y, t)
         return self.geom.sqrt_detB[:, None] * ((vals * self.quad_w) @ self.quad_phi.T)
 
+    def _device_initial(self) -> DeviceState:
+        c = self._c_init.clone()
+        _, u = self._empty_state()
+        u.zero_()
+        self._check(self._lib.qf_velocity(self._ctx, c.data_ptr(), u.data_ptr(), 0,
+                                          len(self.elements), self._stream), "qf_velocity")
+        tdev = self.torch.tensor([0.0, self.dt], dtype=self.torch.float64, device=self.device)
+        return DeviceState(c, u, tdev)
+
+    def lambda_max(self, ds: DeviceState, t: float = 0.0) -> float:
+        """max over owned element edges of the LF speed of a device state."""
+        lam = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device)
+        out, _ = self._empty_state()
+        self._check(self._lib.qf_rhs(self._ctx, ds.c.data_ptr(), ds.u.data_ptr(), float(t), 2,
+                                     out.data_ptr(), lam.data_ptr(), self._stream), "qf_rhs")
+        self._raise_errors("lambda")
+        return float(lam[:, : self.n_own].max().item())
+
     def project_initial(self) -> State:
         """Project analytic (or non-analytic ``initial``) data at t = 0 (solver.py:288-303)."""
+        if self.device_setup:
+            ds = self._device_initial()
+            self._raise_errors("solve_velocity")
+            if not self._dt_fixed:
+                self.dt = float(self.scn.cfl) * self.h_min / self.lambda_max(ds)
+                ds.t_dev[1] = self.dt
+                self._dt_fixed = True
+            return State(t=0.0, _dev=(self, ds))
         c = self.project_fields()[: self.n_own]
         state = State(c=c, u=np.zeros((len(c), 2, self.K)), t=0.0)
         self.solve_velocity(state)

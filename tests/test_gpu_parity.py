@@ -178,3 +178,20 @@ def test_c2_convergence_sweep_gpu():
     print(tab.to_csv())
     assert (eoc[:, 0] > 2.7).all() and (eoc[:, 0] < 3.3).all()
     assert (eoc[:3, 1:] > 2.6).all()
+
+
+@pytest.mark.parametrize("k,case", [(2, "walls"), (3, "walls"), (1, "mms"), (4, "walls")])
+def test_device_setup_matches_host_projection(k, case):
+    """qf_project (device initial + P1 bathymetry projection) == host NumPy setup."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import Discretization
+    mesh = M.build_unit_square_mesh(12, jitter=0.2, seed=3)
+    scn = S.mms_scenario(dt=1e-4) if case == "mms" else S.bump_scenario(seed=0, dt=2e-4, cfl=None)
+    host = Discretization(mesh, scn, k, device_setup=False)
+    dev = Discretization(mesh, scn, k, device_setup=True)
+    assert np.allclose(dev._hb.cpu().numpy(), host._hb.cpu().numpy(), rtol=1e-13, atol=1e-16)
+    a, b = host.project_initial(), dev.project_initial()
+    assert field_rel(b.c, a.c) < 1e-13
+    ra = host.run(host.project_initial(), t_end=5 * scn.dt)
+    rb = dev.run(dev.project_initial(), t_end=5 * scn.dt)
+    assert field_rel(rb.c, ra.c) < 1e-12
