@@ -249,8 +249,9 @@ class Discretization(HostSetup):
     """Mesh + order + scenario bound to device tables (reference solver.py:100-124)."""
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
-                 device: int | None = None, elements=None, n_own: int | None = None):
-        super().__init__(mesh, scenario, order, backend, elements, n_own)
+                 device: int | None = None, elements=None, n_own: int | None = None,
+                 device_setup: bool | None = None):
+        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup)
         self._setup_device(device)
 
     def _setup_device(self, device):
