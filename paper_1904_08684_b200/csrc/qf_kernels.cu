@@ -23,7 +23,6 @@
 #include <string.h>
 
 #include <atomic>
-#include <type_traits>
 #include <string>
 
 #include "../../include/qfswe.h"
@@ -113,45 +112,16 @@ __device__ __forceinline__ void trace_lit(int j, const double* f, double scale, 
   for (int a = 0; a < O::NT; ++a) t[a] = __dmul_rn(t[a], scale);
 }
 
-// rhs accumulator views: registers (double*) for k <= 2, a strided
-// shared-memory column (SRef) for k >= 3 where 3K accumulators would not fit
-// next to the operands of the K^3 volume contraction
-template <int BS>
-struct SRef {
-  double* p;
-  __device__ __forceinline__ double& operator[](int i) const { return p[i * BS]; }
-  __device__ __forceinline__ SRef operator+(int off) const { return SRef{p + off * BS}; }
-};
-
-template <int BS>
-struct SCRef {
-  const double* p;
-  __device__ __forceinline__ double operator[](int i) const { return p[i * BS]; }
-};
-
-// write-sink of the generated volume rows: x[i] = v  ->  r[i] += s * v
-template <class RT>
-struct ScaleAcc {
-  RT r;
-  double s;
-  struct Proxy {
-    RT r;
-    int i;
-    double s;
-    __device__ __forceinline__ void operator=(double v) const { r[i] = fma(s, v, r[i]); }
-  };
-  __device__ __forceinline__ Proxy operator[](int i) const { return Proxy{r, i, s}; }
-};
-
-template <int k>
-struct UseSmemAcc {
-  static constexpr bool value = k >= 3;
-};
-
 // threads (= elements) per block of the stage kernel
+#ifndef QF_BS3
+#define QF_BS3 128
+#endif
+#ifndef QF_BS4
+#define QF_BS4 128
+#endif
 template <int k>
 struct Blk {
-  static constexpr int value = k <= 2 ? 128 : 64;
+  static constexpr int value = k <= 2 ? 128 : (k == 3 ? QF_BS3 : QF_BS4);
 };
 
 // Shared-memory trace exchange.  Phase A: every thread writes its element's
@@ -160,13 +130,13 @@ struct Blk {
 // Phase B: a neighbour inside the block is read from there (no gather, no
 // recomputation); only neighbours outside the block are gathered from global
 // memory and traced.
-template <int k, class RT>
+template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
                                           const double* __restrict__ s_hbm, double B11,
                                           double B12, double B21, double B22, double isd,
-                                          RT r) {
+                                          double* r) {
   using O = Ord<k>;
   constexpr int K = O::K, NT = O::NT, NH = O::NH, BS = Blk<k>::value;
   const int64_t ld = T.ld;
@@ -346,15 +316,20 @@ struct Occ {
 #ifndef QF_OCC2
 #define QF_OCC2 3
 #endif
-  static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : 4);
+#ifndef QF_OCC3
+#define QF_OCC3 2
+#endif
+#ifndef QF_OCC4
+#define QF_OCC4 1
+#endif
+  static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : (k == 3 ? QF_OCC3 : QF_OCC4));
 };
 
 // ---------------------------------------------------------- stage kernel
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 template <int k>
 constexpr size_t stage_smem_bytes() {
-  return sizeof(double) * (Tabs<k>::SIZE + 3 * 6 * Ord<k>::NT * Blk<k>::value + Blk<k>::value +
-                           (UseSmemAcc<k>::value ? 3 * Ord<k>::K * Blk<k>::value : 0));
+  return sizeof(double) * (Tabs<k>::SIZE + 3 * 6 * Ord<k>::NT * Blk<k>::value + Blk<k>::value);
 }
 
 template <int k>
@@ -367,8 +342,6 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double* s_tab = smem;
   double* s_tr = smem + TB::SIZE;
   double* s_hbm = s_tr + 3 * 6 * NT * BS;
-  double* s_r = s_hbm + BS;  // k >= 3: rhs accumulators [3K][BS]
-  constexpr bool PRE = !UseSmemAcc<k>::value;  // preload own data into registers
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
   const int bhi = min(blo + BS, A.e0 + A.n);
@@ -376,183 +349,35 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const bool active = e < bhi;
   const int64_t ld = T.ld;
   const int ee = active ? e : blo;  // inactive threads read a valid element
-  // issue the loads of the element's own data up front: one memory round
+  // issue every load of the element's own data up front: one memory round
   // trip, overlapped with the table copy below
   const double B11 = ldg(T.geo + ee), B12 = ldg(T.geo + ld + ee);
   const double B21 = ldg(T.geo + 2 * ld + ee), B22 = ldg(T.geo + 3 * ld + ee);
   const bool edges = (A.terms & TERM_EDGE) != 0;
   int code[3] = {0, 0, 0};
-  double own_f[PRE ? 6 * K : 1];
+  double own_f[6 * K];
   if (edges) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) code[j] = __ldg(T.nbr + j * ld + ee);
-    if constexpr (PRE) {
 #pragma unroll
-      for (int i = 0; i < 3 * K; ++i) own_f[i] = ldg(A.c + i * ld + ee);
+    for (int i = 0; i < 3 * K; ++i) own_f[i] = ldg(A.c + i * ld + ee);
 #pragma unroll
-      for (int i = 0; i < 2 * K; ++i) own_f[3 * K + i] = ldg(A.u + i * ld + ee);
+    for (int i = 0; i < 2 * K; ++i) own_f[3 * K + i] = ldg(A.u + i * ld + ee);
 #pragma unroll
-      for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
-    }
+    for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
   }
   for (int i = threadIdx.x; i < TB::SIZE; i += BS) s_tab[i] = TB::ptr()[i];
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
 
-  double r_reg[PRE ? 3 * K : 1];
-  using RT = typename std::conditional<PRE, double*, SRef<BS>>::type;
-  RT r;
-  if constexpr (PRE) {
-    r = r_reg;
-  } else {
-    r = SRef<BS>{s_r + slot};
-  }
-  // element-local terms (volume, source, forcing): for k >= 3 they run
-  // before phase A so that their operands can borrow the trace buffer
-  auto element_terms = [&]() {
-#pragma unroll
-    for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
-  {
-    // own data: still in registers from the prologue (k <= 2)
-    double c[3 * K], u[2 * K], hb[K];
-#pragma unroll
-    for (int i = 0; i < 3 * K; ++i) c[i] = (PRE && edges) ? own_f[i % (PRE ? 6 * K : 1)] : ldg(A.c + i * ld + e);
-#pragma unroll
-    for (int i = 0; i < 2 * K; ++i)
-      u[i] = (PRE && edges) ? own_f[(3 * K + i) % (PRE ? 6 * K : 1)] : ldg(A.u + i * ld + e);
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-      hb[i] = (PRE && edges) ? own_f[(5 * K + i) % (PRE ? 6 * K : 1)]
-                             : (i < NH ? ldg(T.hb + i * ld + e) : 0.0);
-    using CT = typename std::conditional<PRE, const double*, SCRef<BS>>::type;
-    CT xi, cU, cV;
-    if constexpr (PRE) {
-      xi = c;
-      cU = c + K;
-      cV = c + 2 * K;
-    } else {  // k >= 3: volume operands in this thread's private smem column
-#pragma unroll
-      for (int i = 0; i < 3 * K; ++i) s_tr[i * BS + slot] = c[i];
-      xi = SCRef<BS>{s_tr + slot};
-      cU = SCRef<BS>{s_tr + K * BS + slot};
-      cV = SCRef<BS>{s_tr + 2 * K * BS + slot};
-    }
-
-    if (QF_EN_VOL && (A.terms & TERM_VOL)) {  // Eqs. (15)-(16), reference solver.py:410-485
-      double al[K], be[K], wv[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        al[i] = B22 * cU[i] - B12 * cV[i];
-        be[i] = -B21 * cU[i] + B11 * cV[i];
-      }
-      O::vol_xi(al, be, ScaleAcc<RT>{r, idet});
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        al[i] = B22 * u[i] - B12 * u[K + i];   // a
-        be[i] = -B21 * u[i] + B11 * u[K + i];  // b
-        wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
-      }
-      const double g = P.g, i32 = idet * isd;
-      O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11,
-                ScaleAcc<RT>{r + K, i32}, ScaleAcc<RT>{r + 2 * K, i32});
-      if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
-        const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          al[i] = B22 * xi[i];
-          be[i] = -B21 * xi[i];
-        }
-        O::vol_xi(al, be, ScaleAcc<RT>{r + K, ghb});
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          al[i] = -B12 * xi[i];
-          be[i] = B11 * xi[i];
-        }
-        O::vol_xi(al, be, ScaleAcc<RT>{r + 2 * K, ghb});
-      }
-    }
-    if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725
-      double d1, d2;
-      O::hb_dref(hb, d1, d2);
-      const double i32 = idet * isd;
-      const double gx = P.g * (B22 * d1 - B21 * d2) * i32, gy = P.g * (-B12 * d1 + B11 * d2) * i32;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
-        r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
-      }
-    }
-  }
-  if (QF_EN_SRC && (A.terms & TERM_SRC) && P.forcing) {
-    // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t) (+ xi mass source), reference :719-724
-    const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
-    double st, ct;
-    sincospi(2.0 * t, &st, &ct);
-    // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
-    // value by a Taylor-evaluated small angle (3 sincospi per element
-    // instead of 3 per quadrature point)
-    const bool tay = P.kind == SCN_MMS && P.taylor;
-    const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
-    double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
-    if (tay) {
-      sincospi(2.0 * (x0 - t), &sx0, &cx0);
-      sincospi(2.0 * (y0 - t), &sy0, &cy0);
-      sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
-    }
-    double fr[3 * K];
-#pragma unroll
-    for (int i = 0; i < 3 * K; ++i) fr[i] = 0.0;
-    QF_UNROLL(QF_QUNROLL)
-    for (int q = 0; q < NQ; ++q) {
-      const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
-      const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
-      double S, Fx, Fy;
-      if (tay) {
-        const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
-        double sz, cz, sw, cw;
-        sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-        sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
-        const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
-        forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
-                    fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
-                    fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
-      } else {
-        forcing(P, x, y, t, st, ct, S, Fx, Fy);
-      }
-      const double* Pq = s_tab + TB::P + q * K;
-#pragma unroll
-      for (int p = 0; p < K; ++p) {
-        const double w = Pq[p];
-        fr[p] = fma(w, S, fr[p]);
-        fr[K + p] = fma(w, Fx, fr[K + p]);
-        fr[2 * K + p] = fma(w, Fy, fr[2 * K + p]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 3 * K; ++i) r[i] = fma(sd, fr[i], r[i]);
-  }
-  };
-  if constexpr (!PRE) {
-    __syncthreads();  // s_tab (quadrature tables) complete
-    if (active) element_terms();
-  }
   if (edges && active) {
     // phase A: own trace moments on all three local edges -> shared memory
-    double t3[NT], fl[K];
+    double t3[NT];
+    s_hbm[slot] = __dmul_rn(__dmul_rn(own_f[5 * K], isd), 0.7071067811865476);
 #pragma unroll
     for (int fi = 0; fi < 6; ++fi) {
-      const double* f;
-      if constexpr (PRE) {
-        f = own_f + fi * K;
-      } else {
-        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld
-                                   : (fi < 5 ? A.u + (int64_t)(fi - 3) * K * ld : T.hb);
-#pragma unroll
-        for (int i = 0; i < K; ++i) fl[i] = (fi < 5 || i < NH) ? ldg(src + i * ld + e) : 0.0;
-        f = fl;
-      }
-      if (fi == 5) s_hbm[slot] = __dmul_rn(__dmul_rn(f[0], isd), 0.7071067811865476);
+      const double* f = own_f + fi * K;
       O::trace0(f, t3);
 #pragma unroll
       for (int a = 0; a < NT; ++a) s_tr[((0 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
@@ -566,7 +391,124 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   }
   __syncthreads();
   if (!active) return;
-  if constexpr (PRE) element_terms();
+
+  double r[3 * K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
+  // own data: still in registers from the prologue when edges are on
+  double c[3 * K], u[2 * K], hb[K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) c[i] = edges ? own_f[i] : ldg(A.c + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) u[i] = edges ? own_f[3 * K + i] : ldg(A.u + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < K; ++i) hb[i] = edges ? own_f[5 * K + i] : (i < NH ? ldg(T.hb + i * ld + e) : 0.0);
+  const double* xi = c;
+  const double* cU = c + K;
+  const double* cV = c + 2 * K;
+
+  if (QF_EN_VOL && (A.terms & TERM_VOL)) {  // Eqs. (15)-(16), reference solver.py:410-485
+    double al[K], be[K], ra[K], rb[K], wv[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = B22 * cU[i] - B12 * cV[i];
+      be[i] = -B21 * cU[i] + B11 * cV[i];
+    }
+    O::vol_xi(al, be, ra);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[i] += ra[i] * idet;
+      al[i] = B22 * u[i] - B12 * u[K + i];   // a
+      be[i] = -B21 * u[i] + B11 * u[K + i];  // b
+      wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
+    }
+    const double g = P.g;
+    O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
+    const double i32 = idet * isd;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] += ra[i] * i32;
+      r[2 * K + i] += rb[i] * i32;
+    }
+    if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+      const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        al[i] = B22 * xi[i];
+        be[i] = -B21 * xi[i];
+      }
+      O::vol_xi(al, be, ra);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        al[i] = -B12 * xi[i];
+        be[i] = B11 * xi[i];
+      }
+      O::vol_xi(al, be, rb);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        r[K + i] += ghb * ra[i];
+        r[2 * K + i] += ghb * rb[i];
+      }
+    }
+  }
+  if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725 (+ xi mass source)
+    double d1, d2;
+    O::hb_dref(hb, d1, d2);
+    const double i32 = idet * isd;
+    const double gx = P.g * (B22 * d1 - B21 * d2) * i32, gy = P.g * (-B12 * d1 + B11 * d2) * i32;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
+      r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
+    }
+    if (P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
+      const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
+      double st, ct;
+      sincospi(2.0 * t, &st, &ct);
+      // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
+      // value by a Taylor-evaluated small angle (2 sincospi per element
+      // instead of 2 per quadrature point)
+      const bool tay = P.kind == SCN_MMS && P.taylor;
+      // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
+      // the centroid; per point only small-angle Taylor rotations follow
+      const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
+      double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
+      if (tay) {
+        sincospi(2.0 * (x0 - t), &sx0, &cx0);
+        sincospi(2.0 * (y0 - t), &sy0, &cy0);
+        sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
+      }
+      QF_UNROLL(QF_QUNROLL)
+      for (int q = 0; q < NQ; ++q) {
+        const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
+        const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+        double S, Fx, Fy;
+        if (tay) {
+          const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
+          double sz, cz, sw, cw;
+          sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+          sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+          const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
+          forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
+                      fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
+                      fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
+        } else {
+          forcing(P, x, y, t, st, ct, S, Fx, Fy);
+        }
+        S *= sd;
+        Fx *= sd;
+        Fy *= sd;
+        const double* Pq = s_tab + TB::P + q * K;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const double w = Pq[p];
+          r[p] = fma(w, S, r[p]);
+          r[K + p] = fma(w, Fx, r[K + p]);
+          r[2 * K + p] = fma(w, Fy, r[2 * K + p]);
+        }
+      }
+    }
+  }
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
 #pragma unroll 1
     for (int j = 0; j < 3; ++j)
@@ -579,7 +521,6 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     return;
   }
   // SSP-RK combination (solver.py:756-764) and velocity of the new state
-  double c[3 * K], hb[K];
   bool fin = true;
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) {
@@ -591,8 +532,6 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = c[i];
   if (!fin) atomicOr(A.err, BIT_NONFINITE);
-#pragma unroll
-  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldv(T.hb + i * ld + e) : 0.0;
   double H[K], uo[K], vo[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) H[i] = c[i] + hb[i];
