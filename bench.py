@@ -122,7 +122,7 @@ class Clocks:
                 "samples": len(self.samples), "reasons": sorted(self.reasons), "source": "nvml"}
 
 
-def cpu_baseline(cfg, budget_s=12.0, n_sample=64, max_steps=None, threads="all"):
+def cpu_baseline(cfg, budget_s=12.0, n_sample=64, max_steps=None, warm=1):
     """Oracle port (dense NumPy restatement of the reference) on this host."""
     from oracle import qfswe_oracle as O
 
@@ -137,7 +137,8 @@ def cpu_baseline(cfg, budget_s=12.0, n_sample=64, max_steps=None, threads="all")
     if scn.cfl is not None:
         _, u = orc.project_initial()
         orc.dt = orc.cfl_dt(scn.cfl, c, u)
-    orc.step(c, 0.0)  # warm-up
+    for _ in range(max(warm, 1)):
+        orc.step(c, 0.0)  # warm-up
     t0 = time.perf_counter()
     steps, t = 0, 0.0
     while True:
@@ -160,16 +161,25 @@ def cpu_baseline(cfg, budget_s=12.0, n_sample=64, max_steps=None, threads="all")
 
 
 def run_reference(args):
+    """Reference arm: the CPU oracle port (dense NumPy restatement of the
+    reference, all host threads) on this config, each step a bounded sample:
+    the same workload on an N_s x N_s mesh with N_s chosen so the whole run
+    stays near two minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cb = cpu_baseline(args.config, max_steps=1)  # one step probe
-    per_step = cb["elapsed_s"]
-    k, n, _, _ = build_problem(args.config)
     t0 = time.perf_counter()
-    for _ in range(args.warmup):
-        pass
-    cbw = cpu_baseline(args.config, max_steps=max(args.steps, 1))
+    probe = cpu_baseline(args.config, n_sample=32, max_steps=1)
+    per_elem_step = probe["elapsed_s"] / (2 * 32 * 32)
+    budget = 120.0 / max(args.steps + args.warmup, 1)
+    n_s = 32
+    for cand in (96, 64, 48):
+        if per_elem_step * 2 * cand * cand <= budget:
+            n_s = cand
+            break
+    cbw = cpu_baseline(args.config, n_sample=n_s, max_steps=max(args.steps, 1),
+                       warm=args.warmup)
+    k, n, _, _ = build_problem(args.config)
     line = {
         "metric": METRIC, "value": cbw["value"], "unit": "DoF-updates/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
@@ -177,11 +187,11 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": CONFIGS[args.config][5], "order": k, "n": n,
-                   "sample_n": 64, "parallelism": "host cores (NumPy/OpenBLAS)"},
+                   "sample_n": n_s, "parallelism": "host cores (NumPy/OpenBLAS)"},
         "cpu_baseline": {k_: cbw[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cbw["value"], "unit": "DoF-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "probe_step_s": per_step, "wall_s": time.perf_counter() - t0,
+        "wall_s": time.perf_counter() - t0,
     }
     print(json.dumps(line), flush=True)
 
@@ -307,26 +317,69 @@ def run_gpu(args):
 
 
 def measure_e2e(disc, st0, steps):
-    """Discretization.step with host states: H2D(c) + step + D2H(c, u) per step."""
+    """End to end through the C ABI with HOST buffers (pinned numpy arrays in the
+    reference's (E, F, K) State layout): every step H2D of c, qf_pack,
+    qf_velocity, qf_step, qf_unpack of (c, u), D2H of (c, u); CUDA events
+    around the whole sequence.  Also reports Discretization.step (the Python
+    API, numpy in/out) wall clock as ``public_api``."""
     import torch
 
+    from paper_1904_08684_b200 import _cabi
     from paper_1904_08684_b200.solver import State
 
-    st = State(st0.c.copy(), st0.u.copy(), st0.t)
-    E, K = disc.mesh.n_triangles, disc.K
-    st = disc.step(st)
-    _ = st.c
+    lib = disc._lib
+    E, K, ld = disc.mesh.n_triangles, disc.K, disc.ld
+    sp = torch.cuda.current_stream().cuda_stream
+    h_c = torch.empty((E, 3, K), dtype=torch.float64).pin_memory()
+    h_out_c = torch.empty((E, 3, K), dtype=torch.float64).pin_memory()
+    h_out_u = torch.empty((E, 2, K), dtype=torch.float64).pin_memory()
+    h_c.numpy()[:] = st0.c
+    d_c = torch.empty((E, 3, K), dtype=torch.float64, device="cuda")
+    d_u = torch.empty((E, 2, K), dtype=torch.float64, device="cuda")
+    c, u = disc._empty_state()
+    c.zero_()
+    u.zero_()
+    tdev = torch.tensor([st0.t, disc.dt], dtype=torch.float64, device="cuda")
+    work = disc._work_buf()
+    pp = disc._perm_ptr(E)
+
+    def one():
+        d_c.copy_(h_c, non_blocking=True)
+        _cabi.check(lib.qf_pack(d_c.data_ptr(), c.data_ptr(), E, 3, K, ld, pp, sp), "pack")
+        _cabi.check(lib.qf_velocity(disc._ctx, c.data_ptr(), u.data_ptr(), 0, -1, sp), "vel")
+        _cabi.check(lib.qf_step(disc._ctx, c.data_ptr(), u.data_ptr(), work.data_ptr(),
+                                tdev.data_ptr(), sp), "step")
+        _cabi.check(lib.qf_unpack(c.data_ptr(), d_c.data_ptr(), E, 3, K, ld, pp, sp), "unpack")
+        _cabi.check(lib.qf_unpack(u.data_ptr(), d_u.data_ptr(), E, 2, K, ld, pp, sp), "unpack")
+        h_out_c.copy_(d_c, non_blocking=True)
+        h_out_u.copy_(d_u, non_blocking=True)
+
+    one()
     torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    ns = stages_of(disc.k)
+    dof = 3 * K * E * ns
+    # the Python API (numpy State in, numpy State out), wall clock
+    st = disc.step(State(st0.c.copy(), st0.u.copy(), st0.t))
+    _ = st.c
     t0 = time.perf_counter()
     for _ in range(steps):
         st = disc.step(State(st.c, st.u, st.t))
-        _ = st.c  # D2H of (c, u)
-    torch.cuda.synchronize()
-    el = time.perf_counter() - t0
-    ns = stages_of(disc.k)
-    return {"value": 3 * K * E * ns * steps / el, "unit": "DoF-updates/s",
+        _ = st.c
+    api = time.perf_counter() - t0
+    return {"value": dof * steps / (ms * 1e-3), "unit": "DoF-updates/s",
             "h2d_bytes_per_step": 8 * 3 * K * E, "d2h_bytes_per_step": 8 * 5 * K * E,
-            "timing": "wall clock around Discretization.step with numpy states"}
+            "timing": "C ABI with pinned host State buffers: H2D c, qf_pack, qf_velocity, "
+                      "qf_step, qf_unpack, D2H (c, u); CUDA events",
+            "public_api": {"value": dof * steps / api, "unit": "DoF-updates/s",
+                           "timing": "Discretization.step with numpy States, wall clock"}}
 
 
 def main():
