@@ -62,6 +62,7 @@ typedef struct qf_desc {
   const int32_t* bnd_elem;  /* [n_bnd] */
   const int32_t* bnd_local; /* [n_bnd] */
   double* ghost;            /* [3][n_bnd][5*(k+2)+6] scratch: exact data per RK stage */
+  double* hbt;              /* [3*(k+1)+1][ld] static h_b edge traces, filled by qf_static */
   /* physics (scenario.py:34-49) */
   double g, f_c, tau_bf;
   int32_t hb_linear;        /* hb_mode == "linear" */
@@ -82,6 +83,10 @@ void qf_destroy(qf_ctx* ctx);
 /* Discretization.solve_velocity (solver.py:315-336): u for elements
  * [e0, e0+n) of state c (n < 0: all owned elements). */
 int qf_velocity(qf_ctx* ctx, const double* c, double* u, int32_t e0, int32_t n, void* stream);
+
+/* Derived static tables (h_b edge traces) from geo and hb for the first n
+ * slots; call after hb is final (qf_project calls it itself). */
+int qf_static(qf_ctx* ctx, int32_t n, void* stream);
 
 /* Device-side setup (project_initial / P1 bathymetry, solver.py:139-168,
  * 282-303): project the field program `prog` (see qf_kernels.cu) onto the

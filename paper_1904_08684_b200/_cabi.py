@@ -17,7 +17,7 @@ BIT_DRY, BIT_SINGULAR, BIT_NONFINITE = 1, 2, 4
 TERM_VOLUME, TERM_EDGE, TERM_SOURCE, TERM_ALL = 1, 2, 4, 7
 
 EXPORTS = (
-    "qf_create", "qf_destroy", "qf_velocity", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
+    "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
     "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill",
     "qf_launch_count", "qf_last_error", "qf_abi_version",
 )
@@ -28,7 +28,7 @@ class QfDesc(C.Structure):
         ("order", C.c_int32), ("n_elem", C.c_int32), ("ld", C.c_int64),
         ("geo", C.c_void_p), ("hb", C.c_void_p), ("nbr", C.c_void_p),
         ("n_bnd", C.c_int32), ("bnd_elem", C.c_void_p), ("bnd_local", C.c_void_p),
-        ("ghost", C.c_void_p),
+        ("ghost", C.c_void_p), ("hbt", C.c_void_p),
         ("g", C.c_double), ("f_c", C.c_double), ("tau_bf", C.c_double),
         ("hb_linear", C.c_int32), ("scn_kind", C.c_int32), ("scn_params", C.c_double * 8),
         ("has_forcing", C.c_int32), ("taylor", C.c_int32), ("block", C.c_int32),
@@ -54,6 +54,7 @@ def load(path: Path | None = None):
         "qf_velocity": (C.c_int, [vp, vp, vp, i32, i32, vp]),
         "qf_ghost": (C.c_int, [vp, d, vp]),
         "qf_project": (C.c_int, [vp, vp, i32, d, vp, vp, vp]),
+        "qf_static": (C.c_int, [vp, i32, vp]),
         "qf_rhs": (C.c_int, [vp, vp, vp, d, i32, vp, vp, vp]),
         "qf_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp]),
         "qf_step": (C.c_int, [vp, vp, vp, vp, vp, vp]),

@@ -27,6 +27,7 @@ struct Tab {
   const double* __restrict__ hb;     // [NH][ld]
   const int* __restrict__ nbr;       // [3][ld]
   const double* __restrict__ ghost;  // [stage][n_bnd][5*NG+6] raw exact data
+  const double* __restrict__ hbt;    // [3*NT+1][ld] static h_b traces (qf_static)
   int64_t ld;
   int n_bnd;
 };

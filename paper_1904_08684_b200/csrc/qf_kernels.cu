@@ -125,16 +125,16 @@ struct Blk {
 };
 
 // Shared-memory trace exchange.  Phase A: every thread writes its element's
-// physical trace moments (xi, U, V, u, v, h_b on local edges 0, 1, 2) to
-// s_tr[((j*6 + f)*NT + a)*BS + slot] and its mean depth term to s_hbm.
+// physical trace moments (xi, U, V, u, v on local edges 0, 1, 2) to
+// s_tr[((j*5 + f)*NT + a)*BS + slot]; the static h_b traces come from the
+// precomputed table T.hbt (qf_static).
 // Phase B: a neighbour inside the block is read from there (no gather, no
 // recomputation); only neighbours outside the block are gathered from global
 // memory and traced.
 template <int k>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
-                                          const double* __restrict__ s_tr,
-                                          const double* __restrict__ s_hbm, double B11,
+                                          const double* __restrict__ s_tr, double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
@@ -149,43 +149,45 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
 
   double own[6][NT], oth[6][NT];
 #pragma unroll
-  for (int f = 0; f < 6; ++f)
+  for (int f = 0; f < 5; ++f)
 #pragma unroll
-    for (int a = 0; a < NT; ++a) own[f][a] = s_tr[((j * 6 + f) * NT + a) * BS + slot];
-  const double hbm_o = s_hbm[slot];
+    for (int a = 0; a < NT; ++a) own[f][a] = s_tr[((j * 5 + f) * NT + a) * BS + slot];
+  // static h_b traces (qf_static): [j*NT + a][ld], mean depth term in row 3*NT
+#pragma unroll
+  for (int a = 0; a < NT; ++a) own[5][a] = ldg(T.hbt + (j * NT + a) * ld + e);
+  const double hbm_o = P.hb_linear ? 0.0 : ldg(T.hbt + 3 * NT * ld + e);
   double hbm_n = hbm_o;
 
   bool dirichlet = false;
   const double* gp = nullptr;
   if (code >= 0) {
     const int nb = code >> 2, jn = code & 3;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) {
+      const double v = ldg(T.hbt + (jn * NT + a) * ld + nb);
+      oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
+    }
+    if (!P.hb_linear) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
     if (nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
       const int ns = nb - blo;
 #pragma unroll
-      for (int f = 0; f < 6; ++f)
+      for (int f = 0; f < 5; ++f)
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          const double v = s_tr[((jn * 6 + f) * NT + a) * BS + ns];
+          const double v = s_tr[((jn * 5 + f) * NT + a) * BS + ns];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
-      hbm_n = s_hbm[ns];
     } else {
       const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
       const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
       const double nisd = rsqrt(det2(nB11, nB12, nB21, nB22));
       double f[K];
 #pragma unroll
-      for (int fi = 0; fi < 6; ++fi) {
-        if (fi < 5) {
-          const double* src =
-              fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+      for (int fi = 0; fi < 5; ++fi) {
+        const double* src =
+            fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
 #pragma unroll
-          for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
-        } else {
-#pragma unroll
-          for (int i = 0; i < K; ++i) f[i] = i < NH ? ldg(T.hb + i * ld + nb) : 0.0;
-          hbm_n = __dmul_rn(__dmul_rn(f[0], nisd), 0.7071067811865476);
-        }
+        for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
         trace_lit<k>(jn, f, nisd, oth[fi]);
 #pragma unroll
         for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
@@ -329,7 +331,7 @@ struct Occ {
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 template <int k>
 constexpr size_t stage_smem_bytes() {
-  return sizeof(double) * (Tabs<k>::SIZE + 3 * 6 * Ord<k>::NT * Blk<k>::value + Blk<k>::value);
+  return sizeof(double) * (3 * 5 * Ord<k>::NT * Blk<k>::value);
 }
 
 template <int k>
@@ -339,9 +341,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   using TB = Tabs<k>;
   constexpr int K = O::K, NH = O::NH, NQ = O::NQ, NT = O::NT, BS = Blk<k>::value;
   extern __shared__ double smem[];
-  double* s_tab = smem;
-  double* s_tr = smem + TB::SIZE;
-  double* s_hbm = s_tr + 3 * 6 * NT * BS;
+  double* s_tr = smem;  // trace exchange [3 edges][5 fields][NT][BS]
+  const double* s_tab = TB::ptr();  // per-order constants (constant memory, uniform reads)
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
   const int bhi = min(blo + BS, A.e0 + A.n);
@@ -366,7 +367,6 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #pragma unroll
     for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
   }
-  for (int i = threadIdx.x; i < TB::SIZE; i += BS) s_tab[i] = TB::ptr()[i];
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
@@ -374,19 +374,18 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if (edges && active) {
     // phase A: own trace moments on all three local edges -> shared memory
     double t3[NT];
-    s_hbm[slot] = __dmul_rn(__dmul_rn(own_f[5 * K], isd), 0.7071067811865476);
 #pragma unroll
-    for (int fi = 0; fi < 6; ++fi) {
+    for (int fi = 0; fi < 5; ++fi) {
       const double* f = own_f + fi * K;
       O::trace0(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((0 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((0 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
       O::trace1(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((1 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((1 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
       O::trace2(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((2 * 6 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((2 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
     }
   }
   __syncthreads();
@@ -512,8 +511,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
 #pragma unroll 1
     for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_hbm, B11, B12, B21, B22, isd,
-                   r);
+      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, B11, B12, B21, B22, isd, r);
   }
   if (A.mode == 0) {
 #pragma unroll
@@ -697,6 +695,33 @@ __global__ void project_kernel(Tab T, Phys P, const double* __restrict__ prog, i
   if (dry) atomicOr(err, BIT_DRY);
 }
 
+// Static per-element-edge data derived from geometry and bathymetry:
+// hbt[j*NT + a][e] = physical h_b trace moments on local edge j (the
+// bathymetry part of every edge flux, read by both sides of the edge), and
+// hbt[3*NT][e] = element-mean depth term of hb_mode="const".
+template <int k>
+__global__ void static_kernel(Tab T, int n, double* __restrict__ hbt) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NT = O::NT, NH = O::NH;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int64_t ld = T.ld;
+  const double isd = rsqrt(det2(T.geo[e], T.geo[ld + e], T.geo[2 * ld + e], T.geo[3 * ld + e]));
+  double f[K], t3[NT];
+#pragma unroll
+  for (int i = 0; i < K; ++i) f[i] = i < NH ? T.hb[i * ld + e] : 0.0;
+  O::trace0(f, t3);
+#pragma unroll
+  for (int a = 0; a < NT; ++a) hbt[(0 * NT + a) * ld + e] = __dmul_rn(t3[a], isd);
+  O::trace1(f, t3);
+#pragma unroll
+  for (int a = 0; a < NT; ++a) hbt[(1 * NT + a) * ld + e] = __dmul_rn(t3[a], isd);
+  O::trace2(f, t3);
+#pragma unroll
+  for (int a = 0; a < NT; ++a) hbt[(2 * NT + a) * ld + e] = __dmul_rn(t3[a], isd);
+  hbt[3 * NT * ld + e] = __dmul_rn(__dmul_rn(f[0], isd), 0.7071067811865476);
+}
+
 __global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
 
 __global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
@@ -814,6 +839,13 @@ static void launch_ghost(qf_ctx* x, double t, const double* t_dev, int nstage, d
 }
 
 template <int k>
+static void launch_static(qf_ctx* x, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  static_kernel<k><<<(n + 127) / 128, 128, 0, s>>>(x->tab, n, x->d.hbt);
+  g_launches++;
+}
+
+template <int k>
 static void launch_project(qf_ctx* x, const double* prog, int n, double h_min, double* c,
                            double* hb) {
   if (n <= 0) return;
@@ -832,14 +864,14 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
   if (!d || !out) return fail(QF_E_ARG, "null argument");
   if (d->order < 0 || d->order > 4) return fail(QF_E_ARG, "order must be in 0..4");
   if (d->n_elem < 0 || d->ld < d->n_elem || d->ld % 32) return fail(QF_E_ARG, "bad n_elem/ld");
-  if (!d->geo || !d->hb || !d->nbr) return fail(QF_E_ARG, "missing static tables");
+  if (!d->geo || !d->hb || !d->nbr || !d->hbt) return fail(QF_E_ARG, "missing static tables");
   if (d->n_bnd > 0 && (!d->bnd_elem || !d->bnd_local || !d->ghost))
     return fail(QF_E_ARG, "missing Dirichlet boundary tables");
   qf_ctx* x = new qf_ctx();
   x->d = *d;
   x->K = (d->order + 1) * (d->order + 2) / 2;
   x->NT = d->order + 1;
-  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->ld, d->n_bnd};
+  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->hbt, d->ld, d->n_bnd};
   x->phys.g = d->g;
   x->phys.fc = d->f_c;
   x->phys.tau = d->tau_bf;
@@ -874,11 +906,18 @@ int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, vo
   return cuda_check("velocity_kernel");
 }
 
+int qf_static(qf_ctx* x, int32_t n, void* stream) {
+  if (!x) return fail(QF_E_ARG, "null ctx");
+  QF_DISPATCH(x->d.order, launch_static, x, n, (cudaStream_t)stream);
+  return cuda_check("static_kernel");
+}
+
 int qf_project(qf_ctx* x, const double* prog, int32_t n, double h_min, double* c, double* hb,
                void* stream) {
   if (!x || !prog || !c || !hb) return fail(QF_E_ARG, "null argument");
   x->stream_hint = (cudaStream_t)stream;
   QF_DISPATCH(x->d.order, launch_project, x, prog, n, h_min, c, hb);
+  QF_DISPATCH(x->d.order, launch_static, x, n, (cudaStream_t)stream);
   return cuda_check("project_kernel");
 }
 

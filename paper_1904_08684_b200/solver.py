@@ -283,6 +283,8 @@ class Discretization(HostSetup):
         d.n_bnd = nb
         d.bnd_elem, d.bnd_local = self._bel.data_ptr(), self._bloc.data_ptr()
         d.ghost = self._ghost.data_ptr()
+        self._hbt = torch.zeros((3 * (self.k + 1) + 1, ld), dtype=torch.float64, device=dev)
+        d.hbt = self._hbt.data_ptr()
         d.g, d.f_c, d.tau_bf = scn.g, scn.f_c, scn.tau_bf
         d.hb_linear = 1 if scn.hb_mode == "linear" else 0
         d.scn_kind = scn.device.kind
@@ -296,6 +298,8 @@ class Discretization(HostSetup):
         self._ctx = ctx
         self._lib = lib
         self._work = None
+        if not self.device_setup:
+            self._check(lib.qf_static(ctx, len(self.elements), self._stream), "qf_static")
         if self.device_setup:
             self._prog = torch.from_numpy(self.scn.field_program()).to(dev)
             c0, _ = self._empty_state()
