@@ -46,6 +46,9 @@ namespace qf {
 #ifndef QF_EN_EDGE
 #define QF_EN_EDGE 1
 #endif
+#ifndef QF_EUNROLL
+#define QF_EUNROLL 1
+#endif
 #ifndef QF_QUNROLL
 #define QF_QUNROLL 1
 #endif
@@ -113,6 +116,9 @@ __device__ __forceinline__ void trace_lit(int j, const double* f, double scale, 
 }
 
 // threads (= elements) per block of the stage kernel
+#ifndef QF_BS2
+#define QF_BS2 128
+#endif
 #ifndef QF_BS3
 #define QF_BS3 128
 #endif
@@ -121,7 +127,7 @@ __device__ __forceinline__ void trace_lit(int j, const double* f, double scale, 
 #endif
 template <int k>
 struct Blk {
-  static constexpr int value = k <= 2 ? 128 : (k == 3 ? QF_BS3 : QF_BS4);
+  static constexpr int value = k <= 1 ? 128 : (k == 2 ? QF_BS2 : (k == 3 ? QF_BS3 : QF_BS4));
 };
 
 // Shared-memory trace exchange.  Phase A: every thread writes its element's
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     }
   }
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
-#pragma unroll 1
+    QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < 3; ++j)
       edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, B11, B12, B21, B22, isd, r);
   }
