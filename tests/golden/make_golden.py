@@ -162,6 +162,15 @@ def main():
     terms = stage_terms(disc, st0, 0.0)
     st = disc.step(disc.step(st0))
     np.savez_compressed(HERE / "ring_k1.npz", c0=st0.c, c2=st.c, **terms)
+    # H. hb_mode = "const" (paper-form bathymetry, solver.py:498-510, 606-608)
+    for k in (1, 2):
+        scn = R.scenario.perturbed_square_scenario(dt=0.5, hb_mode="const")
+        disc = R.solver.Discretization(mesh, scn, k)
+        st0 = disc.project_initial()
+        sr = perturbed_state(disc, st0, 300 + k)
+        terms = stage_terms(disc, sr, 1.3)
+        st = disc.step(disc.step(st0))
+        np.savez_compressed(HERE / f"const_k{k}.npz", cr=sr.c, ur=sr.u, c2=st.c, **terms)
     # G. MMS convergence sweeps (reference errors for the EOC tests)
     for k, ns, dt, steps in ((1, (8, 16, 32), 1e-4, 200), (2, (8, 16), 2e-5, 200),
                              (3, (4, 8), 2e-5, 100)):

@@ -195,3 +195,58 @@ def test_device_setup_matches_host_projection(k, case):
     ra = host.run(host.project_initial(), t_end=5 * scn.dt)
     rb = dev.run(dev.project_initial(), t_end=5 * scn.dt)
     assert field_rel(rb.c, ra.c) < 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_const_hb_mode_vs_reference(golden, k):
+    """hb_mode='const' (paper-form bathymetry term) against the reference."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import State
+    g = golden(f"const_k{k}.npz")
+    disc = _disc(M.build_square_mesh(3, 0.2, 42), S.perturbed_square_scenario(dt=0.5,
+                                                                             hb_mode="const"), k)
+    sr = State(g["cr"].copy(), g["ur"].copy(), 0.0)
+    assert field_rel(disc.element_rhs(sr), g["elem"]) < TOL
+    assert field_rel(disc.edge_rhs(sr, 1.3), g["edge"]) < TOL
+    assert rel_l2(disc.compute_lambda(sr, 1.3), g["lam"]) < TOL
+    out = disc.run(disc.project_initial(), t_end=1.0)
+    assert field_rel(out.c, g["c2"]) < TOL
+
+
+def test_error_semantics():
+    """DryState / SingularProjection / FloatingPointError raised like the reference."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import DryState, SingularProjection, State
+    disc = _disc(M.build_square_mesh(2, 0.0, 0), S.lake_at_rest_scenario(dt=0.5), 1)
+    st = disc.project_initial()
+    bad = State(st.c.copy(), st.u.copy(), 0.0)
+    bad.c[3, 0, 0] = -50.0  # negative depth on one element
+    with pytest.raises(DryState):
+        disc.rhs(bad, 0.0)
+    sing = State(st.c.copy(), st.u.copy(), 0.0)
+    sing.c[:, 0, :] = 0.0
+    hbc = disc.hb_coef
+    sing.c[:, 0, :] = -hbc  # H == 0 identically -> singular projection
+    with pytest.raises(SingularProjection):
+        disc.solve_velocity(sing)
+    nan = State(st.c.copy(), st.u.copy(), 0.0)
+    nan.c[5, 1, 0] = np.nan
+    with pytest.raises((FloatingPointError, ArithmeticError)):
+        disc.step(nan)
+    # a good state still steps after the errors were cleared
+    out = disc.step(st)
+    assert np.isfinite(out.c).all()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+def test_tiny_and_ragged_meshes(n):
+    """E not a multiple of the block / warp size, single-quad meshes."""
+    from oracle import qfswe_oracle as O
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    mesh = M.build_unit_square_mesh(n)
+    disc = _disc(mesh, S.mms_scenario(dt=1e-4), 2)
+    orc = O.OracleSolver(O.OMesh(mesh.vertices, mesh.triangles), O.mms_baseline(dt=1e-4), 2)
+    c0, _ = orc.project_initial()
+    ref, _, _ = orc.run(c0, 0.0, 3)
+    out = disc.run(disc.project_initial(), t_end=3e-4)
+    assert field_rel(out.c, ref) < TOL
