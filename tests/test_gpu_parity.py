@@ -220,7 +220,7 @@ def test_error_semantics():
     disc = _disc(M.build_square_mesh(2, 0.0, 0), S.lake_at_rest_scenario(dt=0.5), 1)
     st = disc.project_initial()
     bad = State(st.c.copy(), st.u.copy(), 0.0)
-    bad.c[3, 0, 0] = -50.0  # negative depth on one element
+    bad.c[3, 0, 0] = -10.0 * disc.geom.sqrt_detB[3]  # xi ~ -14: negative depth on one element
     with pytest.raises(DryState):
         disc.rhs(bad, 0.0)
     sing = State(st.c.copy(), st.u.copy(), 0.0)
