@@ -137,14 +137,14 @@ struct Blk {
 // Phase B: a neighbour inside the block is read from there (no gather, no
 // recomputation); only neighbours outside the block are gathered from global
 // memory and traced.
-template <int k>
+template <int k, int BS = Blk<k>::value>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr, double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
-  constexpr int K = O::K, NT = O::NT, NH = O::NH, BS = Blk<k>::value;
+  constexpr int K = O::K, NT = O::NT, NH = O::NH;
   const int64_t ld = T.ld;
   // own outward normal: physical image of the reference edge direction
   const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
