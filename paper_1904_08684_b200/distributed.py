@@ -261,7 +261,8 @@ class DistributedRunner(PartitionRunner):
             hmin = torch.tensor([self.disc.h_min], dtype=torch.float64, device="cuda")
             dist.all_reduce(lmax, op=dist.ReduceOp.MAX)
             dist.all_reduce(hmin, op=dist.ReduceOp.MIN)
-            self.dt = float(scenario.cfl) * float(hmin.item()) / float(lmax.item())
+            from .solver import cfl_time_step
+            self.dt = cfl_time_step(scenario.cfl, order, float(hmin.item()), float(lmax.item()))
         self.comm = torch.cuda.Stream()
 
     def step(self):

@@ -30,7 +30,8 @@ from .scenario import KIND_NONE, Scenario
 from .symbolic import build_basis
 from .tensors import build_ref_tensors, triangle_rule
 
-__all__ = ["DryState", "SingularProjection", "State", "Discretization", "flux_dot_n"]
+__all__ = ["DryState", "SingularProjection", "State", "Discretization", "flux_dot_n",
+           "cfl_time_step"]
 
 XI, U, V = 0, 1, 2
 
@@ -41,6 +42,18 @@ class DryState(ArithmeticError):
 
 class SingularProjection(ArithmeticError):
     """Per-element velocity projection system is numerically singular."""
+
+
+def cfl_time_step(cfl: float, k: int, h_min: float, lam_max: float) -> float:
+    """CFL time step of the BASELINE C3-C5 runs (the reference has none).
+
+    dt = cfl * h_min / ((2k + 1) * lambda_max), with h_min the reference's
+    min(detB / longest edge) (solver.py:240-246) and lambda_max the largest
+    Lax-Friedrichs speed at t = 0.  The 1/(2k+1) factor is the usual DG
+    stability scaling (without it, k = 4 / SSP-RK3 at cfl = 0.1 blows up in
+    ~10 steps in both the oracle and the GPU path).
+    """
+    return float(cfl) * h_min / ((2 * k + 1) * lam_max)
 
 
 def flux_dot_n(xi, Uq, Vq, uu, uv, hb, n1, n2, g):
@@ -445,7 +458,7 @@ class Discretization(HostSetup):
             ds = self._device_initial()
             self._raise_errors("solve_velocity")
             if not self._dt_fixed:
-                self.dt = float(self.scn.cfl) * self.h_min / self.lambda_max(ds)
+                self.dt = cfl_time_step(self.scn.cfl, self.k, self.h_min, self.lambda_max(ds))
                 ds.t_dev[1] = self.dt
                 self._dt_fixed = True
             return State(t=0.0, _dev=(self, ds))
@@ -458,9 +471,9 @@ class Discretization(HostSetup):
         return state
 
     def cfl_dt(self, state: State) -> float:
-        """dt = cfl * h_min / max lambda(t) (extension)."""
+        """dt = cfl * h_min / ((2k + 1) max lambda(t)) (extension)."""
         lam = self.compute_lambda(state, state.t)
-        return float(self.scn.cfl) * self.h_min / float(lam.max())
+        return cfl_time_step(self.scn.cfl, self.k, self.h_min, float(lam.max()))
 
     # --------------------------------------------------------- operators
     def solve_velocity(self, state: State) -> None:
