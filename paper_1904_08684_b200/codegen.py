@@ -42,8 +42,31 @@ def lit(v: float) -> str:
     return s
 
 
+# Constant pool of the order being generated.  Coefficients are emitted as
+# references P{k}[i] into a __constant__ array with compile-time indices, so
+# ptxas feeds them to DFMA/DMUL as constant-bank operands (c[0x3][...])
+# instead of materialising each 64-bit literal with two UMOV/IMAD.MOV.
+_POOL: dict | None = None
+_POOL_NAME = "P"
+
+
+def coef(v: float) -> str:
+    """Pool reference for |v| (callers handle the sign)."""
+    v = abs(float(v))
+    if _POOL is None:
+        return lit(v)
+    if v not in _POOL:
+        _POOL[v] = len(_POOL)
+    return f"{_POOL_NAME}[{_POOL[v]}]"
+
+
+def scoef(v: float) -> str:
+    """Signed pool reference."""
+    return coef(v) if v >= 0 else f"-{coef(v)}"
+
+
 def _sum(terms: list[tuple[float, str]]) -> str:
-    """Literal linear combination; +-1 coefficients folded."""
+    """Linear combination with pooled coefficients; +-1 folded."""
     if not terms:
         return "0.0"
     out = []
@@ -55,10 +78,10 @@ def _sum(terms: list[tuple[float, str]]) -> str:
             t = x
             sign = "-"
         elif c < 0:
-            t = f"{lit(-c)} * {x}"
+            t = f"{coef(c)} * {x}"
             sign = "-"
         else:
-            t = f"{lit(c)} * {x}"
+            t = f"{coef(c)} * {x}"
             sign = "+"
         if i == 0:
             out.append(t if sign == "+" else f"-{t}")
@@ -83,11 +106,12 @@ def gen_order(k: int) -> str:
     gs, gw = edge_rule(2 * (k + 2) - 1)
     NG = len(gw)
     phi_q = np.array([[f.eval(x, y) for (x, y) in qp] for f in basis.functions])  # (K, NQ)
+    global _POOL, _POOL_NAME
+    # measured per order (round 1): pooled constants win for k = 0, 1, 2, 4;
+    # for k = 3 literals give ptxas a better register allocation
+    _POOL, _POOL_NAME = ({} if k != 3 else None), f"qf_pool{k}"
     L = []
     w = L.append
-    w(f"// Generated by paper_1904_08684_b200/codegen.py for order k={k}. Do not edit.")
-    w("#pragma once")
-    w("namespace qf {")
     w(f"template <> struct Ord<{k}> {{")
     w(f"  static constexpr int K = {K}, NT = {NT}, NH = {NH}, NQ = {NQ}, NG = {NG};")
     # ---- velocity matrix
@@ -172,9 +196,9 @@ def gen_order(k: int) -> str:
                 w(f"    t[{a}] = 0.0;")
                 continue
             c0, i0 = terms[0]
-            expr = f"__dmul_rn({lit(c0)}, f[{i0}])"
+            expr = f"__dmul_rn({scoef(c0)}, f[{i0}])"
             for c, i in terms[1:]:
-                expr = f"__fma_rn({lit(c)}, f[{i}], {expr})"
+                expr = f"__fma_rn({scoef(c)}, f[{i}], {expr})"
             w(f"    t[{a}] = {expr};")
         w("  }")
         w(f"  template <class RT> static __device__ __forceinline__ void lift{j}(const double* F, double s, RT r) {{")
@@ -246,6 +270,16 @@ def gen_order(k: int) -> str:
         w("    }")
     w("  }")
     w("};")
+    pool = sorted((_POOL or {}).items(), key=lambda kv: kv[1])
+    _POOL = None
+    head = [f"// Generated by paper_1904_08684_b200/codegen.py for order k={k}. Do not edit.",
+            "#pragma once", "namespace qf {",
+            f"__constant__ double qf_pool{k}[{max(len(pool), 1)}] = {{"]
+    vals = [lit(v) for v, _ in pool] or ["0.0"]
+    for i0 in range(0, len(vals), 4):
+        head.append("  " + ", ".join(vals[i0:i0 + 4]) + ",")
+    head.append("};")
+    L[:0] = head
     # ---- tables for the looped (non-unrolled) edge and quadrature code:
     # Lam[3][K][NT] | QX[NQ] | QY[NQ] | P[NQ][K] (P = w_q phi_p(q)) | GS[NG] |
     # GPSI[NT][NG] (psi_a(s_g) w_g, Dirichlet ghost moments) | PHI[NQ][K] (phi_p(q))
