@@ -40,7 +40,7 @@ CONFIGS = {
 }
 # dram__bytes_read.sum + dram__bytes_write.sum of one stage_kernel launch
 # (stage 1 after the L2 flush) from `ncu --set full`, profiles/r01_*
-PROFILED_TRAFFIC = {"c2": 45.4e6}
+PROFILED_TRAFFIC = {"c2": 57.9e6}
 METRIC = "DG DoF-updates/s per RK stage (p=1..4) at 1/2/4/8 B200; % of HBM roofline"
 
 
