@@ -79,6 +79,7 @@ struct StageArgs {
   double t, toff, dt, a, b;
   int e0, n, terms, mode;
   int gstage;                     // Dirichlet ghost table of this stage
+  const double* vol;              // k >= 3: precomputed volume rhs [3K][ld] (volume_kernel)
 };
 
 // ---------------------------------------------------------------- edges
@@ -333,6 +334,60 @@ struct Occ {
   static constexpr int value = k <= 1 ? 4 : (k == 2 ? QF_OCC2 : (k == 3 ? QF_OCC3 : QF_OCC4));
 };
 
+// Volume terms, Eqs. (15)-(16) (reference solver.py:410-485, const-h_b form
+// :498-510): factorised stiffness-triple contraction in literal code.
+template <int k>
+__device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B12, double B21,
+                                             double B22, double isd, double idet,
+                                             const double* xi, const double* cU,
+                                             const double* cV, const double* u,
+                                             const double* hb, double* r) {
+  using O = Ord<k>;
+  constexpr int K = O::K;
+    double al[K], be[K], ra[K], rb[K], wv[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    al[i] = B22 * cU[i] - B12 * cV[i];
+    be[i] = -B21 * cU[i] + B11 * cV[i];
+  }
+  O::vol_xi(al, be, ra);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    r[i] += ra[i] * idet;
+    al[i] = B22 * u[i] - B12 * u[K + i];   // a
+    be[i] = -B21 * u[i] + B11 * u[K + i];  // b
+    wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
+  }
+  const double g = P.g;
+  O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
+  const double i32 = idet * isd;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    r[K + i] += ra[i] * i32;
+    r[2 * K + i] += rb[i] * i32;
+  }
+  if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+    const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = B22 * xi[i];
+      be[i] = -B21 * xi[i];
+    }
+    O::vol_xi(al, be, ra);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = -B12 * xi[i];
+      be[i] = B11 * xi[i];
+    }
+    O::vol_xi(al, be, rb);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] += ghb * ra[i];
+      r[2 * K + i] += ghb * rb[i];
+    }
+  }
+}
+
 // ---------------------------------------------------------- stage kernel
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 template <int k>
@@ -412,49 +467,12 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double* cU = c + K;
   const double* cV = c + 2 * K;
 
-  if (QF_EN_VOL && (A.terms & TERM_VOL)) {  // Eqs. (15)-(16), reference solver.py:410-485
-    double al[K], be[K], ra[K], rb[K], wv[K];
+  if constexpr (k <= 2) {
+    if (QF_EN_VOL && (A.terms & TERM_VOL))
+      volume_terms<k>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
+  } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      al[i] = B22 * cU[i] - B12 * cV[i];
-      be[i] = -B21 * cU[i] + B11 * cV[i];
-    }
-    O::vol_xi(al, be, ra);
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      r[i] += ra[i] * idet;
-      al[i] = B22 * u[i] - B12 * u[K + i];   // a
-      be[i] = -B21 * u[i] + B11 * u[K + i];  // b
-      wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
-    }
-    const double g = P.g;
-    O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
-    const double i32 = idet * isd;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      r[K + i] += ra[i] * i32;
-      r[2 * K + i] += rb[i] * i32;
-    }
-    if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
-      const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        al[i] = B22 * xi[i];
-        be[i] = -B21 * xi[i];
-      }
-      O::vol_xi(al, be, ra);
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        al[i] = -B12 * xi[i];
-        be[i] = B11 * xi[i];
-      }
-      O::vol_xi(al, be, rb);
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        r[K + i] += ghb * ra[i];
-        r[2 * K + i] += ghb * rb[i];
-      }
-    }
+    for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
   }
   if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725 (+ xi mass source)
     double d1, d2;
@@ -545,6 +563,34 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     A.u_out[i * ld + e] = uo[i];
     A.u_out[(K + i) * ld + e] = vo[i];
   }
+}
+
+// k >= 3: the volume contraction as its own launch (the fused stage kernel
+// would otherwise spill its K^3-operand working set); writes vol[3K][ld].
+template <int k>
+__global__ void __launch_bounds__(128) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
+                                                     const double* __restrict__ u, int e0, int n,
+                                                     double* __restrict__ vol) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NH = O::NH;
+  const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e0 + n) return;
+  const int64_t ld = T.ld;
+  const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
+  const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
+  const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), idet = isd * isd;
+  double cc[3 * K], uu[2 * K], hb[K], r[3 * K];
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) uu[i] = ldg(u + i * ld + e);
+#pragma unroll
+  for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
+  volume_terms<k>(P, B11, B12, B21, B22, isd, idet, cc, cc + K, cc + 2 * K, uu, hb, r);
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) vol[i * ld + e] = r[i];
 }
 
 template <int k>
@@ -784,6 +830,7 @@ struct qf_ctx {
   const void* gkey[4] = {nullptr, nullptr, nullptr, nullptr};
   int graph_launches = 0;
   cudaStream_t stream_hint = nullptr;
+  double* vol = nullptr;  // k >= 3 volume-rhs scratch [3K][ld] (context-owned)
 };
 
 static thread_local std::string g_last_error;
@@ -810,7 +857,16 @@ static int cuda_check(const char* what) {
   }
 
 template <int k>
-static void launch_stage(qf_ctx* x, const StageArgs& a, cudaStream_t s) {
+static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
+  StageArgs a = a_in;
+  if constexpr (k >= 3) {
+    if ((a.terms & TERM_VOL) && a.n > 0) {
+      volume_kernel<k><<<(a.n + 127) / 128, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n,
+                                                         x->vol);
+      g_launches++;
+      a.vol = x->vol;
+    }
+  }
   constexpr int bs = Blk<k>::value;
   constexpr size_t smem = stage_smem_bytes<k>();
   static bool attr = false;
@@ -886,6 +942,11 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
   x->phys.forcing = d->has_forcing;
   x->phys.taylor = d->taylor;
   for (int i = 0; i < 8; ++i) x->phys.p[i] = d->scn_params[i];
+  if (d->order >= 3 &&
+      cudaMalloc(&x->vol, sizeof(double) * 3 * x->K * (size_t)d->ld) != cudaSuccess) {
+    delete x;
+    return fail(QF_E_CUDA, "cudaMalloc(volume scratch) failed");
+  }
   if (cudaMalloc(&x->err, sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {
     delete x;
@@ -898,6 +959,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
 void qf_destroy(qf_ctx* x) {
   if (!x) return;
   if (x->graph) cudaGraphExecDestroy(x->graph);
+  if (x->vol) cudaFree(x->vol);
   cudaFree(x->err);
   delete x;
 }
@@ -1050,7 +1112,7 @@ int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* 
 
 static int kernels_per_step(qf_ctx* x) {
   const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
-  return stages + (x->d.n_bnd > 0 ? 1 : 0) + 1;
+  return stages * (x->d.order >= 3 ? 2 : 1) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
 }
 
 int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
