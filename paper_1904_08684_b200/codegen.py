@@ -33,6 +33,7 @@ from .tensors import (LAMBDA_SAMPLES, build_ref_tensors, build_trace_space, edge
 
 GEN_DIR = Path(__file__).resolve().parent / "csrc" / "generated"
 TOL = 1e-15
+QF_LITERAL_ORDERS = tuple(int(x) for x in __import__("os").environ.get("QF_LITERAL_ORDERS", "3").split(",") if x)
 
 
 def lit(v: float) -> str:
@@ -109,7 +110,7 @@ def gen_order(k: int) -> str:
     global _POOL, _POOL_NAME
     # measured per order (round 1): pooled constants win for k = 0, 1, 2, 4;
     # for k = 3 literals give ptxas a better register allocation
-    _POOL, _POOL_NAME = ({} if k != 3 else None), f"qf_pool{k}"
+    _POOL, _POOL_NAME = ({} if k not in QF_LITERAL_ORDERS else None), f"qf_pool{k}"
     L = []
     w = L.append
     w(f"template <> struct Ord<{k}> {{")
