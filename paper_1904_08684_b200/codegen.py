@@ -184,6 +184,38 @@ def gen_order(k: int) -> str:
             w("      }")
         w(f"      rU[{p}] = su; rV[{p}] = sv; }}")
     w("  }")
+    # ---- U/V rows, input-outer order (volume_kernel, k >= 3): only a, b, wv
+    # and the accumulators stay live; cU_i, cV_i, xi_i are fetched once each
+    # (the caller pre-scales them by 1/(detB sqrt(detB)) through its view).
+    w("  template <class RT, class CT> static __device__ __forceinline__ void vol_uv_acc(CT cU, CT cV,"
+      " CT xi, const double* a, const double* b, const double* wv,")
+    w("      double g22, double g21, double g12, double g11, RT rU, RT rV) {")
+    for i in range(K):
+        w(f"    {{ const double ci = cU[{i}], vi = cV[{i}], xq = xi[{i}];")
+        for p in range(K):
+            zt = [(rt.T[0, p, i, m], f"a[{m}]") for m in range(K) if _nz(rt.T[0, p, i, m])]
+            zt += [(rt.T[1, p, i, m], f"b[{m}]") for m in range(K) if _nz(rt.T[1, p, i, m])]
+            y1 = [(rt.T[0, p, i, m], f"wv[{m}]") for m in range(K) if _nz(rt.T[0, p, i, m])]
+            y2 = [(rt.T[1, p, i, m], f"wv[{m}]") for m in range(K) if _nz(rt.T[1, p, i, m])]
+            if not (zt or y1 or y2):
+                continue
+            w("      {")
+            if zt:
+                w(f"        const double z = {_sum(zt)};")
+                w(f"        rU[{p}] = fma(z, ci, rU[{p}]); rV[{p}] = fma(z, vi, rV[{p}]);")
+            if y1 and y2:
+                w(f"        const double y1 = {_sum(y1)}, y2 = {_sum(y2)};")
+                w(f"        rU[{p}] = fma(xq, fma(g22, y1, -g21 * y2), rU[{p}]);")
+                w(f"        rV[{p}] = fma(xq, fma(g11, y2, -g12 * y1), rV[{p}]);")
+            elif y1:
+                w(f"        const double y1 = {_sum(y1)};")
+                w(f"        rU[{p}] = fma(xq * g22, y1, rU[{p}]); rV[{p}] = fma(-xq * g12, y1, rV[{p}]);")
+            elif y2:
+                w(f"        const double y2 = {_sum(y2)};")
+                w(f"        rU[{p}] = fma(-xq * g21, y2, rU[{p}]); rV[{p}] = fma(xq * g11, y2, rV[{p}]);")
+            w("      }")
+        w("    }")
+    w("  }")
     # ---- traces and lifts
     for j in range(3):
         # explicit fma chains: the same trace is evaluated by the element's own
