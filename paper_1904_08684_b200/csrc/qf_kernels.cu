@@ -417,16 +417,21 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double B21 = ldg(T.geo + 2 * ld + ee), B22 = ldg(T.geo + 3 * ld + ee);
   const bool edges = (A.terms & TERM_EDGE) != 0;
   int code[3] = {0, 0, 0};
-  double own_f[6 * K];
+  // k <= 2: the element's own data is loaded once up front and stays in
+  // registers; for k >= 3 (6K values) each phase re-reads it (L1/L2)
+  constexpr bool PRE = k <= 2;
+  double own_f[PRE ? 6 * K : 1];
   if (edges) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) code[j] = __ldg(T.nbr + j * ld + ee);
+    if constexpr (PRE) {
 #pragma unroll
-    for (int i = 0; i < 3 * K; ++i) own_f[i] = ldg(A.c + i * ld + ee);
+      for (int i = 0; i < 3 * K; ++i) own_f[i] = ldg(A.c + i * ld + ee);
 #pragma unroll
-    for (int i = 0; i < 2 * K; ++i) own_f[3 * K + i] = ldg(A.u + i * ld + ee);
+      for (int i = 0; i < 2 * K; ++i) own_f[3 * K + i] = ldg(A.u + i * ld + ee);
 #pragma unroll
-    for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
+      for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
+    }
   }
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
@@ -434,10 +439,18 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 
   if (edges && active) {
     // phase A: own trace moments on all three local edges -> shared memory
-    double t3[NT];
+    double t3[NT], fl[PRE ? 1 : K];
 #pragma unroll
     for (int fi = 0; fi < 5; ++fi) {
-      const double* f = own_f + fi * K;
+      const double* f;
+      if constexpr (PRE) {
+        f = own_f + fi * K;
+      } else {
+        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+        for (int i = 0; i < K; ++i) fl[i] = ldv(src + i * ld + e);
+        f = fl;
+      }
       O::trace0(f, t3);
 #pragma unroll
       for (int a = 0; a < NT; ++a) s_tr[((0 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
@@ -458,11 +471,14 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   // own data: still in registers from the prologue when edges are on
   double c[3 * K], u[2 * K], hb[K];
 #pragma unroll
-  for (int i = 0; i < 3 * K; ++i) c[i] = edges ? own_f[i] : ldg(A.c + i * ld + e);
+  for (int i = 0; i < 3 * K; ++i)
+    c[i] = (PRE && edges) ? own_f[PRE ? i : 0] : ldv(A.c + i * ld + e);
 #pragma unroll
-  for (int i = 0; i < 2 * K; ++i) u[i] = edges ? own_f[3 * K + i] : ldg(A.u + i * ld + e);
+  for (int i = 0; i < 2 * K; ++i)
+    u[i] = (PRE && edges) ? own_f[PRE ? 3 * K + i : 0] : ldv(A.u + i * ld + e);
 #pragma unroll
-  for (int i = 0; i < K; ++i) hb[i] = edges ? own_f[5 * K + i] : (i < NH ? ldg(T.hb + i * ld + e) : 0.0);
+  for (int i = 0; i < K; ++i)
+    hb[i] = (PRE && edges) ? own_f[PRE ? 5 * K + i : 0] : (i < NH ? ldv(T.hb + i * ld + e) : 0.0);
   const double* xi = c;
   const double* cU = c + K;
   const double* cV = c + 2 * K;
