@@ -199,7 +199,7 @@ class PartitionRunner:
         self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own)
         d = self.disc
         self.K, self.ld, self.lib = d.K, d.ld, d._lib
-        self.c = d.upload_fields(d.project_fields())
+        self.c = d._c_init.clone() if d.device_setup else d.upload_fields(d.project_fields())
         self.u = torch.zeros_like(self.c[:2])
         self.bufs = {0: (self.c, self.u),
                      1: (torch.zeros_like(self.c), torch.zeros_like(self.u)),
@@ -240,6 +240,8 @@ class PartitionRunner:
 
     def end_step(self):
         if self.k == 0:
+            self.torch.cuda.current_stream().wait_stream(getattr(self, "comm", None)
+                                                         or self.torch.cuda.current_stream())
             self.c.copy_(self.bufs[1][0])
             self.u.copy_(self.bufs[1][1])
         self.t += self.dt

@@ -369,9 +369,8 @@ class Discretization(HostSetup):
     def _upload_c(self, c_host: np.ndarray):
         t = self.torch
         E = len(c_host)
-        a = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64))
-        if self.device.type == "cuda":
-            a = a.pin_memory()
+        # torch's caching host allocator keeps the pinned staging buffer
+        a = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64)).pin_memory()
         a = a.to(self.device, non_blocking=True)
         c, _ = self._empty_state()
         c.zero_()
