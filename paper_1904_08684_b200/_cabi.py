@@ -10,7 +10,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqfswe.so"
+import os
+
+# QF_LIB: diagnostic override (tools/variants.py builds knob variants there)
+LIB_PATH = Path(os.environ.get("QF_LIB") or Path(__file__).resolve().parent / "_lib" / "libqfswe.so")
 
 QF_OK, QF_E_DRY, QF_E_SINGULAR, QF_E_NONFINITE, QF_E_CUDA, QF_E_ARG = range(6)
 BIT_DRY, BIT_SINGULAR, BIT_NONFINITE = 1, 2, 4

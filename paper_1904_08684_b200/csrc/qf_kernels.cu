@@ -322,6 +322,10 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
 
 template <int k>
 struct Occ {
+// orders >= QF_VSPLIT solve the velocity of the new state in its own launch
+#ifndef QF_VSPLIT
+#define QF_VSPLIT 5
+#endif
 #ifndef QF_OCC2
 #define QF_OCC2 3
 #endif
@@ -469,13 +473,15 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
   // own data: still in registers from the prologue when edges are on
-  double c[3 * K], u[2 * K], hb[K];
+  // (u is an operand of the volume terms only, which k >= 3 takes from A.vol)
+  double c[3 * K], u[PRE ? 2 * K : 1], hb[K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i)
     c[i] = (PRE && edges) ? own_f[PRE ? i : 0] : ldv(A.c + i * ld + e);
+  if constexpr (PRE) {
 #pragma unroll
-  for (int i = 0; i < 2 * K; ++i)
-    u[i] = (PRE && edges) ? own_f[PRE ? 3 * K + i : 0] : ldv(A.u + i * ld + e);
+    for (int i = 0; i < 2 * K; ++i) u[i] = edges ? own_f[3 * K + i] : ldv(A.u + i * ld + e);
+  }
 #pragma unroll
   for (int i = 0; i < K; ++i)
     hb[i] = (PRE && edges) ? own_f[PRE ? 5 * K + i : 0] : (i < NH ? ldv(T.hb + i * ld + e) : 0.0);
@@ -570,6 +576,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = c[i];
   if (!fin) atomicOr(A.err, BIT_NONFINITE);
+  if constexpr (k >= QF_VSPLIT) return;  // velocity_kernel follows (register pressure)
   double H[K], uo[K], vo[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) H[i] = c[i] + hb[i];
@@ -956,6 +963,13 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   if (grid == 0) return;
   stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
   g_launches++;
+  if constexpr (k >= QF_VSPLIT) {
+    if (a.mode == 1) {
+      velocity_kernel<k><<<(a.n + 127) / 128, 128, 0, s>>>(x->tab, a.c_out, a.u_out, a.e0, a.n,
+                                                        x->err);
+      g_launches++;
+    }
+  }
 }
 
 template <int k>
@@ -1190,7 +1204,7 @@ int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* 
 
 static int kernels_per_step(qf_ctx* x) {
   const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
-  return stages * (x->d.order >= 3 ? 2 : 1) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
+  return stages * (1 + (x->d.order >= 3) + (x->d.order >= QF_VSPLIT)) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
 }
 
 int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
