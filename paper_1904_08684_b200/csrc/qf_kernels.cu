@@ -324,7 +324,7 @@ template <int k>
 struct Occ {
 // orders >= QF_VSPLIT solve the velocity of the new state in its own launch
 #ifndef QF_VSPLIT
-#define QF_VSPLIT 5
+#define QF_VSPLIT 3
 #endif
 #ifndef QF_OCC2
 #define QF_OCC2 3
@@ -598,8 +598,11 @@ struct GRow {
   __device__ __forceinline__ double operator[](int i) const { return s * ldv(p + i * ld); }
 };
 
+#ifndef QF_VOCC
+#define QF_VOCC 1
+#endif
 template <int k>
-__global__ void __launch_bounds__(128) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
+__global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
                                                      const double* __restrict__ u, int e0, int n,
                                                      double* __restrict__ vol) {
   using O = Ord<k>;

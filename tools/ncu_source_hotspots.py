@@ -1,5 +1,7 @@
 import csv, collections, subprocess, sys
-out = subprocess.run(["ncu","-i",sys.argv[1],"--page","source","--csv","--print-source","cuda,sass"],capture_output=True,text=True).stdout
+import os
+flt = ["-k", os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+out = subprocess.run(["ncu","-i",sys.argv[1],*flt,"--page","source","--csv","--print-source","cuda,sass"],capture_output=True,text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 cur_file = None; hdr=None
 agg = collections.defaultdict(lambda: [0,0,""])

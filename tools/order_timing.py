@@ -12,7 +12,7 @@ from paper_1904_08684_b200.solver import Discretization  # noqa: E402
 from tools.term_timing import timed  # noqa: E402
 
 
-def main(n=256, orders=(1, 2, 3, 4), scen="bumps"):
+def main(n=256, orders=(1, 2, 3, 4), scen="bumps", once=False):
     mesh = M.build_unit_square_mesh(n)
     for k in orders:
         scn = S.bump_scenario(seed=0, cfl=0.1) if scen == "bumps" else S.mms_scenario(dt=2e-5)
@@ -24,11 +24,22 @@ def main(n=256, orders=(1, 2, 3, 4), scen="bumps"):
                                   w.data_ptr(), w[3 * disc.K * disc.ld:].data_ptr(), 0.5, 0.5,
                                   0.0, disc.dt, None, 0.0, 0, -1, s)
         st()
+        if once:  # for ncu launch lists: one more stage, no timing loop
+            st()
+            torch.cuda.synchronize()
+            continue
         us = timed(st, 20)
         dof = 3 * disc.K * mesh.n_triangles
         print(f"k={k} N={n} E={mesh.n_triangles} {scen}: {us:8.1f} us/stage  {dof / us * 1e6:.3e} DoF/s")
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 256,
-         scen=sys.argv[2] if len(sys.argv) > 2 else "bumps")
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("n", nargs="?", type=int, default=256)
+    ap.add_argument("scen", nargs="?", default="bumps")
+    ap.add_argument("--orders", default="1,2,3,4")
+    ap.add_argument("--once", action="store_true")
+    a = ap.parse_args()
+    main(a.n, tuple(int(x) for x in a.orders.split(",")), a.scen, a.once)
