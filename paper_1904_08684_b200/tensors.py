@@ -21,10 +21,12 @@ Gauss-Legendre on the triangle, Gauss-Legendre on [0, 1]).
 
 from __future__ import annotations
 
+import csv
 import math
 from dataclasses import dataclass
 from fractions import Fraction
 from functools import lru_cache
+from pathlib import Path
 
 import numpy as np
 
@@ -289,3 +291,89 @@ def edge_point(edge: int, s):
     x0, x1s, y0, y1s = EDGE_MAPS[edge]
     s = np.asarray(s, dtype=float)
     return x0 + x1s * s, y0 + y1s * s
+
+
+# ------------------------------------------------- verification and dumps
+
+@dataclass(frozen=True)
+class TensorReport:
+    """Deviation of the frozen tensors from quadrature (reference tensors.py:200-204)."""
+
+    order: int
+    max_abs_dev: float
+    max_rel_dev: float
+
+
+def verify_tensors(t: RefTensors) -> TensorReport:
+    """Re-derive every tensor with degree-exact floating quadrature and report
+    the largest deviation (reference tensors.py:207-254; relative deviations
+    are scaled by the largest entry of each tensor)."""
+    k = t.order
+    basis = build_basis(k)
+    K = basis.size
+    pts, wts = triangle_rule(3 * k + 1)
+    x1, x2 = pts[:, 0], pts[:, 1]
+    vals = np.array([f.eval(x1, x2) for f in basis.functions])                     # [i, q]
+    grads = np.array([[basis.gradients[i][l].eval(x1, x2) * np.ones_like(x1) for l in range(2)]
+                      for i in range(K)])                                          # [i, l, q]
+    sq, wq = edge_rule(3 * k)
+    tr = np.array([[f.eval(*edge_point(e, sq)) * np.ones_like(sq) for f in basis.functions]
+                   for e in range(3)])                                             # [e, i, q]
+    trr = np.array([[f.eval(*edge_point(e, 1.0 - sq)) * np.ones_like(sq) for f in basis.functions]
+                    for e in range(3)])
+    quad = {
+        "M": np.einsum("pq,iq,q->pi", vals, vals, wts),
+        "S": np.einsum("plq,iq,q->lpi", grads, vals, wts),
+        "T": np.einsum("plq,iq,mq,q->lpim", grads, vals, vals, wts),
+        "G": np.einsum("pq,iq,mq,q->pim", vals, vals, vals, wts),
+        "E": np.einsum("epq,eiq,q->epi", tr, tr, wq),
+        "EX": np.einsum("epq,fiq,q->efpi", tr, trr, wq),
+        "ET": np.einsum("epq,eiq,emq,q->epim", tr, tr, tr, wq),
+        "ETX": np.einsum("epq,fiq,fmq,q->efpim", tr, trr, trr, wq),
+    }
+    max_abs = max_rel = 0.0
+    for name, frozen in t.as_dict().items():
+        dev = float(np.abs(frozen - quad[name]).max())
+        max_abs = max(max_abs, dev)
+        scale = float(np.abs(quad[name]).max())
+        max_rel = max(max_rel, dev / scale if scale > 0.0 else dev)  # k = 0: S = T = 0
+    return TensorReport(order=k, max_abs_dev=max_abs, max_rel_dev=max_rel)
+
+
+_CSV_INDEX = {
+    "M": ["p", "i"], "S": ["l", "p", "i"], "T": ["l", "p", "i", "m"], "G": ["p", "i", "m"],
+    "E": ["e", "p", "i"], "EX": ["e", "eN", "p", "i"], "ET": ["e", "p", "i", "m"],
+    "ETX": ["e", "eN", "p", "i", "m"],
+}
+
+
+def dump_tensors_csv(t: RefTensors, out_dir) -> list:
+    """One CSV per tensor, ``<name>_k<order>.csv``, header = index names +
+    ``value``, entries in C order with %.17g (reference tensors.py:257-275)."""
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    paths = []
+    for name, arr in t.as_dict().items():
+        path = out_dir / f"{name}_k{t.order}.csv"
+        idx = np.indices(arr.shape).reshape(arr.ndim, -1).T
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(_CSV_INDEX[name] + ["value"])
+            w.writerows([*map(int, row), f"{v:.17g}"] for row, v in zip(idx, arr.ravel()))
+        paths.append(path)
+    return paths
+
+
+def load_tensors_csv(order: int, in_dir) -> RefTensors:
+    """Inverse of dump_tensors_csv (shapes from the order)."""
+    ref = build_ref_tensors(order)
+    arrs = {}
+    for name, arr in ref.as_dict().items():
+        out = np.zeros(arr.shape)
+        with open(Path(in_dir) / f"{name}_k{order}.csv", newline="") as fh:
+            rd = csv.reader(fh)
+            next(rd)
+            for row in rd:
+                out[tuple(int(v) for v in row[:-1])] = float(row[-1])
+        arrs[name] = out
+    return RefTensors(order=order, **arrs)

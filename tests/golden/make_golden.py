@@ -101,8 +101,27 @@ def perturbed_state(disc, state, seed):
     return s
 
 
+def tensor_files(R):
+    """verify_tensors reports and SHA-256 of every dump_tensors_csv file, k = 0..3."""
+    import hashlib
+    import tempfile
+
+    out = {}
+    for k in range(4):
+        t = R.tensors.build_ref_tensors(k)
+        if k > 0:  # the reference's verify_tensors divides by max|S| = 0 at k = 0
+            rep = R.tensors.verify_tensors(t)
+            out[f"report_k{k}"] = np.array([rep.max_abs_dev, rep.max_rel_dev])
+        with tempfile.TemporaryDirectory() as d:
+            for path in R.tensors.dump_tensors_csv(t, d):
+                out[f"sha_{path.stem}"] = np.array(hashlib.sha256(path.read_bytes()).hexdigest())
+    np.savez_compressed(HERE / "tensor_files.npz", **out)
+
+
 def main():
     R = load_reference()
+    if "--tensor-files" in sys.argv:
+        return tensor_files(R)
     # A. tensors
     for k in range(4):
         t = R.tensors.build_ref_tensors(k)

@@ -64,6 +64,31 @@ def test_tensors_bit_identical_to_reference(golden, k):
         assert np.array_equal(t.as_dict()[name], g[name]), name
 
 
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_tensor_csv_dump_byte_identical_to_reference(golden, tmp_path, k):
+    """dump_tensors_csv writes the reference's files byte for byte
+    (reference tensors.py:257-275); load_tensors_csv inverts it."""
+    import hashlib
+    g = golden("tensor_files.npz")
+    t = T.build_ref_tensors(k)
+    for path in T.dump_tensors_csv(t, tmp_path):
+        assert hashlib.sha256(path.read_bytes()).hexdigest() == str(g[f"sha_{path.stem}"]), path.name
+    back = T.load_tensors_csv(k, tmp_path)
+    for name, x in t.as_dict().items():
+        assert np.array_equal(x, back.as_dict()[name]), name
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_verify_tensors_report(golden, k):
+    """verify_tensors (reference tensors.py:207-254): frozen vs quadrature at
+    roundoff, same magnitude as the reference's own report."""
+    rep = T.verify_tensors(T.build_ref_tensors(k))
+    assert rep.order == k and rep.max_rel_dev < 1e-13
+    if k <= 3:
+        ref_abs, ref_rel = golden("tensor_files.npz")[f"report_k{k}"]
+        assert rep.max_abs_dev < 10 * ref_abs + 1e-15 and rep.max_rel_dev < 10 * ref_rel + 1e-16
+
+
 def test_p4_tensors_vs_quadrature():
     from oracle import qfswe_oracle as O
     a, b = T.build_ref_tensors(4), O.build_tensors(4)
