@@ -317,7 +317,10 @@ def gen_order(k: int) -> str:
     # Lam[3][K][NT] | QX[NQ] | QY[NQ] | P[NQ][K] (P = w_q phi_p(q)) | GS[NG] |
     # GPSI[NT][NG] (psi_a(s_g) w_g, Dirichlet ghost moments) | PHI[NQ][K] (phi_p(q))
     gpsi = np.array([[float(legendre01(a, gs[g])) * gw[g] for g in range(NG)] for a in range(NT)])
-    tab = list(ts.Lam.ravel()) + list(qp[:, 0]) + list(qp[:, 1]) + \
+    # (entries the literal trace code skips are zeroed, so a table-driven
+    # trace reproduces its bits)
+    lam_t = np.where(np.abs(ts.Lam) > TOL, ts.Lam, 0.0)
+    tab = list(lam_t.ravel()) + list(qp[:, 0]) + list(qp[:, 1]) + \
         list((phi_q * qw[None, :]).T.ravel()) + list(gs) + list(gpsi.ravel()) + \
         list(phi_q.T.ravel())
     w(f"__constant__ double c_tab{k}[{len(tab)}] = {{")

@@ -138,10 +138,25 @@ struct Blk {
 // Phase B: a neighbour inside the block is read from there (no gather, no
 // recomputation); only neighbours outside the block are gathered from global
 // memory and traced.
+// out-of-block neighbour traces computed cooperatively per block (phase A2)
+#ifndef QF_HCAP
+#define QF_HCAP 64
+#endif
+// timing experiments only (wrong numerics): in-block traces for every neighbour
+#ifndef QF_FAKE_HALO
+#define QF_FAKE_HALO 0
+#endif
+#ifndef QF_NOFALLBACK
+#define QF_NOFALLBACK 0
+#endif
+#ifndef QF_FAKE_HBT
+#define QF_FAKE_HBT 0
+#endif
 template <int k, int BS = Blk<k>::value>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
-                                          const double* __restrict__ s_tr, double B11,
+                                          const double* __restrict__ s_tr,
+                                          const double* __restrict__ s_ht, int hslot, double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
@@ -171,12 +186,12 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     const int nb = code >> 2, jn = code & 3;
 #pragma unroll
     for (int a = 0; a < NT; ++a) {
-      const double v = ldg(T.hbt + (jn * NT + a) * ld + nb);
+      const double v = QF_FAKE_HBT ? own[5][a] : ldg(T.hbt + (jn * NT + a) * ld + nb);
       oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
     }
     if (!P.hb_linear) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
-    if (nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
-      const int ns = nb - blo;
+    if (QF_FAKE_HALO || (nb >= blo && nb < bhi)) {  // neighbour traced by its own thread in phase A
+      const int ns = QF_FAKE_HALO ? ((nb - blo) & (BS - 1)) : nb - blo;
 #pragma unroll
       for (int f = 0; f < 5; ++f)
 #pragma unroll
@@ -184,20 +199,30 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
           const double v = s_tr[((jn * 5 + f) * NT + a) * BS + ns];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
-    } else {
-      const double nB11 = ldg(T.geo + nb), nB12 = ldg(T.geo + ld + nb);
-      const double nB21 = ldg(T.geo + 2 * ld + nb), nB22 = ldg(T.geo + 3 * ld + nb);
-      const double nisd = rsqrt(det2(nB11, nB12, nB21, nB22));
-      double f[K];
+    } else if (QF_NOFALLBACK || hslot >= 0) {  // out-of-block neighbour, traced in phase A2
+#pragma unroll
+      for (int f = 0; f < 5; ++f)
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+          const double v = s_ht[(f * NT + a) * QF_HCAP + (QF_NOFALLBACK ? max(hslot, 0) : hslot)];
+          oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
+        }
+    } else {  // request list overflow (rare): gather and trace here, compact code
+      const double nisd = rsqrt(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
+                                     ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
+      const double* L = s_ht + 5 * NT * QF_HCAP + jn * K * NT;  // s_L (stage_kernel layout)
 #pragma unroll
       for (int fi = 0; fi < 5; ++fi) {
         const double* src =
             fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
 #pragma unroll
-        for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
-        trace_lit<k>(jn, f, nisd, oth[fi]);
-#pragma unroll
-        for (int a = 1; a < NT; a += 2) oth[fi][a] = -oth[fi][a];  // s -> 1-s
+        for (int a = 0; a < NT; ++a) {
+          double acc = 0.0;
+#pragma unroll 1
+          for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], ldg(src + i * ld + nb), acc);
+          const double v = __dmul_rn(acc, nisd);
+          oth[fi][a] = (a & 1) ? -v : v;  // s -> 1-s
+        }
       }
     }
   } else {
@@ -320,12 +345,12 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   }
 }
 
-template <int k>
-struct Occ {
 // orders >= QF_VSPLIT solve the velocity of the new state in its own launch
 #ifndef QF_VSPLIT
 #define QF_VSPLIT 3
 #endif
+template <int k>
+struct Occ {
 #ifndef QF_OCC2
 #define QF_OCC2 3
 #endif
@@ -396,7 +421,9 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 template <int k>
 constexpr size_t stage_smem_bytes() {
-  return sizeof(double) * (3 * 5 * Ord<k>::NT * Blk<k>::value);
+  constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
+  return sizeof(double) * (3 * 5 * NT * Blk<k>::value + 5 * NT * QF_HCAP + 3 * K * NT) +
+         sizeof(int) * (QF_HCAP + 1);
 }
 
 template <int k>
@@ -405,8 +432,12 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   using O = Ord<k>;
   using TB = Tabs<k>;
   constexpr int K = O::K, NH = O::NH, NQ = O::NQ, NT = O::NT, BS = Blk<k>::value;
+  constexpr int HC = QF_HCAP;
   extern __shared__ double smem[];
   double* s_tr = smem;  // trace exchange [3 edges][5 fields][NT][BS]
+  double* s_ht = s_tr + 3 * 5 * NT * BS;  // out-of-block neighbour traces [5][NT][HC]
+  double* s_L = s_ht + 5 * NT * HC;       // Lambda [3][K][NT] (neighbour edge varies by lane)
+  int* s_req = reinterpret_cast<int*>(s_L + 3 * K * NT);  // [HC] neighbour codes, then count
   const double* s_tab = TB::ptr();  // per-order constants (constant memory, uniform reads)
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
@@ -440,6 +471,10 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
+  if (edges) {
+    if (slot == 0) s_req[HC] = 0;
+    for (int i = slot; i < 3 * K * NT; i += BS) s_L[i] = s_tab[TB::L + i];
+  }
 
   if (edges && active) {
     // phase A: own trace moments on all three local edges -> shared memory
@@ -467,6 +502,47 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     }
   }
   __syncthreads();
+  // phase A2: traces of out-of-block neighbours on the shared edge, one
+  // (neighbour, edge) request per thread instead of a divergent gather inside
+  // the edge loop; same rounding sequence as the owner's phase A
+  int hs[3] = {-1, -1, -1};
+  if (edges) {
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int nb = code[j] >> 2;
+        if (code[j] >= 0 && (nb < blo || nb >= bhi)) {
+          const int h = atomicAdd(s_req + HC, 1);
+          if (h < HC) {
+            s_req[h] = code[j];
+            hs[j] = h;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nh = min(s_req[HC], HC);
+    // one (request, field) item per thread
+    for (int it = slot; it < 5 * nh; it += BS) {
+      const int h = it / 5, fi = it - 5 * h;
+      const int cd = s_req[h], nb = cd >> 2, jn = cd & 3;
+      const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+      double f[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
+      const double nisd = rsqrt(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
+                                     ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
+      const double* L = s_L + jn * K * NT;
+#pragma unroll
+      for (int a = 0; a < NT; ++a) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], f[i], acc);
+        s_ht[(fi * NT + a) * HC + h] = __dmul_rn(acc, nisd);
+      }
+    }
+    __syncthreads();
+  }
   if (!active) return;
 
   double r[3 * K];
@@ -557,7 +633,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
     QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, B11, B12, B21, B22, isd, r);
+      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], B11, B12, B21, B22,
+                   isd, r);
   }
   if (A.mode == 0) {
 #pragma unroll

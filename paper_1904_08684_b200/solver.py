@@ -136,11 +136,17 @@ class HostSetup:
     DEVICE_SETUP_MIN = 1_000_000
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
-                 elements=None, n_own: int | None = None, device_setup: bool | None = None):
+                 elements=None, n_own: int | None = None, device_setup: bool | None = None,
+                 slot_order: str = "locality"):
         """``elements``/``n_own`` restrict the discretization to a partition
         (``distributed.py``): local order = owned elements then halo copies.
         ``device_setup`` moves the initial / bathymetry projections to the GPU
-        (``qf_project``; default: automatic for large meshes)."""
+        (``qf_project``; default: automatic for large meshes).  ``slot_order``:
+        device element slots in Z-order ("locality", default) or mesh order
+        ("natural"; results are identical, only the memory locality differs)."""
+        if slot_order not in ("locality", "natural"):
+            raise ValueError("slot_order must be 'locality' or 'natural'")
+        self.slot_order = slot_order
         if backend not in ("einsum", "ir"):
             raise ValueError("backend must be 'einsum' or 'ir'")
         if scenario.hb_mode not in ("linear", "const"):
@@ -175,7 +181,7 @@ class HostSetup:
             self._setup_bathymetry()
         # device slot order: locality (Z-order) permutation of the local rows
         # for a whole mesh; a partition's local order is already sorted
-        self.perm = None if self.partitioned else locality_order(mesh)
+        self.perm = None if self.partitioned or self.slot_order == "natural" else locality_order(mesh)
         slots = self.elements if self.perm is None else self.elements[self.perm]
         self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
                                    slots, self.n_own)
@@ -263,8 +269,8 @@ class Discretization(HostSetup):
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
                  device: int | None = None, elements=None, n_own: int | None = None,
-                 device_setup: bool | None = None):
-        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup)
+                 device_setup: bool | None = None, slot_order: str = "locality"):
+        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup, slot_order)
         self._setup_device(device)
 
     def _setup_device(self, device):

@@ -38,9 +38,20 @@ def run(orders, n, scen):
         print(f"[{so.stem}]\n    {out or r.stderr[-800:]}", flush=True)
 
 
+def execute(cmd):
+    """Run a shell command once per variant with QF_LIB pointing at it."""
+    for so in sorted(VAR.glob("*.so")):
+        r = subprocess.run(cmd, shell=True, env=dict(os.environ, QF_LIB=str(so)),
+                           capture_output=True, text=True, cwd=ROOT)
+        out = (r.stdout.strip() or r.stderr[-800:]).replace("\n", "\n    ")
+        print(f"[{so.stem}]\n    {out}", flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2:])
+    elif sys.argv[1] == "exec":
+        execute(" ".join(sys.argv[2:]))
     else:
         run(",".join(sys.argv[2].split()) if len(sys.argv) > 2 else "3,4",
             int(sys.argv[3]) if len(sys.argv) > 3 else 256,
