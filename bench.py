@@ -38,9 +38,21 @@ CONFIGS = {
     "c4": (2, 2048, "bumps", None, 0.2, "C4 jittered bumps+walls p=2 N=2048 SSP-RK3 CFL 0.1"),
     "c5": (4, 1448, "bumps", None, 0.0, "C5 weak bumps+walls p=4 N=1448/GPU SSP-RK3 CFL 0.1"),
 }
-# dram__bytes_read.sum + dram__bytes_write.sum of one stage_kernel launch
-# (stage 1 after the L2 flush) from `ncu --set full`, profiles/r01_*
-PROFILED_TRAFFIC = {"c2": 57.9e6}
+# Per RK stage (averaged over the stages of one L2-flushed step) of the stage
+# launches (stage_kernel, + volume_kernel + velocity_kernel for k >= 3):
+# DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) and FP64 FLOP per
+# element (2 dfma + dmul + dadd, smsp__sass_thread_inst_executed_op_*), from
+# tools/kernel_counts.sh under ncu; summaries in profiles/r01_kernel_counts.txt
+PROFILED = {
+    "c1": {"bytes_per_elem": 322.4, "flop_per_elem": 3201.2},
+    "c2": {"bytes_per_elem": 538.9, "flop_per_elem": 6294.8},
+    "c3": {"bytes_per_elem": 2337.7, "flop_per_elem": 8467.7},
+    "c4": {"bytes_per_elem": 735.2, "flop_per_elem": 3369.9},
+    "c5": {"bytes_per_elem": 3637.8, "flop_per_elem": 20723.1},
+}
+# FP64 FMA-pipe peak of this B200, measured by tools/micro/fp64_pipes.cu
+# (DFMA 35.3 TF/s, DMMA 37.1 TF/s, one shared pipe; profiles/r01_fp64_pipes.txt)
+FP64_PEAK_TFLOPS = 35.3
 METRIC = "DG DoF-updates/s per RK stage (p=1..4) at 1/2/4/8 B200; % of HBM roofline"
 
 
@@ -289,6 +301,13 @@ def run_gpu(args):
     bytes_step = sum(E * alg_bytes_per_elem(K, r) for r in rvec)
     kern_ms_step = float(st.sum(axis=1).mean())
     achieved = bytes_step / (kern_ms_step * 1e-3) / 1e9
+    prof = PROFILED.get(args.config) if args.n is None else None
+    fp64 = None
+    if prof:
+        tf = prof["flop_per_elem"] * E * ns / (kern_ms_step * 1e-3) / 1e12
+        fp64 = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tf / FP64_PEAK_TFLOPS, "flop_per_elem_stage": prof["flop_per_elem"],
+                "peak_source": "measured DFMA throughput (tools/micro/fp64_pipes.cu)"}
     e2e = measure_e2e(disc, st0, max(3, min(args.steps, 20)))
     cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
     line = {
@@ -303,10 +322,17 @@ def run_gpu(args):
                    "dof_per_stage": 3 * K * E, "l2": "flushed (256 MB write) between timed steps",
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": PROFILED_TRAFFIC.get(args.config),
-                     "peak_source": peak_src, "kernel": "stage_kernel",
+                     "frac": achieved / peak,
+                     "traffic": prof["bytes_per_elem"] * E if prof else None,
+                     "traffic_note": "DRAM bytes per stage launch (ncu, averaged over the "
+                                     "stages of an L2-flushed step), algorithmic: "
+                                     f"{bytes_step / ns:.4g}",
+                     "peak_source": peak_src,
+                     "kernel": "stage_kernel" if k <= 2 else
+                               "stage (volume_kernel + stage_kernel + velocity_kernel)",
                      "kernel_ms_per_step": kern_ms_step, "alg_bytes_per_step": bytes_step,
-                     "kernel_share_of_step": kern_ms_step / (total_ms / args.steps)},
+                     "kernel_share_of_step": kern_ms_step / (total_ms / args.steps),
+                     "fp64": fp64},
         "hbm_roofline_dof_per_s": 3 * K * E * ns / (bytes_step / (peak * 1e9)),
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -423,7 +423,7 @@ template <int k>
 constexpr size_t stage_smem_bytes() {
   constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
   return sizeof(double) * (3 * 5 * NT * Blk<k>::value + 5 * NT * QF_HCAP + 3 * K * NT) +
-         sizeof(int) * (QF_HCAP + 1);
+         sizeof(int) * (QF_HCAP + 8);
 }
 
 template <int k>
@@ -471,9 +471,73 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
+  // out-of-block neighbour requests, (neighbour, its edge) codes in per-warp
+  // slot ranges (ballot prefix, no shared counter); hs[j] = slot or -1
+  constexpr int NW = BS / 32, WC = HC / NW;
+  int* s_cnt = s_req + HC;  // [NW] requests per warp
+  int hs[3] = {-1, -1, -1};
   if (edges) {
-    if (slot == 0) s_req[HC] = 0;
     for (int i = slot; i < 3 * K * NT; i += BS) s_L[i] = s_tab[TB::L + i];
+    const int lane = slot & 31, w = slot >> 5;
+    int base = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int nb = code[j] >> 2;
+      const bool req = active && code[j] >= 0 && (nb < blo || nb >= bhi);
+      const unsigned m = __ballot_sync(0xffffffffu, req);
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      if (req && pos < WC) {
+        s_req[w * WC + pos] = code[j];
+        hs[j] = w * WC + pos;
+      }
+      base += __popc(m);
+    }
+    if (lane == 0) s_cnt[w] = min(base, WC);
+  }
+  // phase A2 work items: (request, field) pairs in request order; item `it`
+  // -> request slot / field
+  auto item = [&](int it, int& hsl, int& fi) {
+    int le = it / 5, w = 0;
+    fi = it - 5 * le;
+    while (w < NW - 1 && le >= s_cnt[w]) le -= s_cnt[w++];
+    hsl = w * WC + le;
+  };
+  auto a2_trace = [&](int hsl, int fi, const double* f, const double* g4) {
+    const int cd = s_req[hsl], jn = cd & 3;
+    const double nisd = rsqrt(det2(g4[0], g4[1], g4[2], g4[3]));
+    const double* L = s_L + jn * K * NT;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], f[i], acc);
+      s_ht[(fi * NT + a) * HC + hsl] = __dmul_rn(acc, nisd);
+    }
+  };
+  auto a2_load = [&](int hsl, int fi, double* f, double* g4) {
+    const int nb = s_req[hsl] >> 2;
+    const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+    for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g4[i] = ldg(T.geo + i * ld + nb);
+  };
+  int nit = 0;
+  // k <= 2: the first A2 item's loads are issued before phase A (one exposed
+  // memory latency per block instead of two)
+  constexpr bool PF = k <= 2;
+  double pf[PF ? K : 1], pg[4];
+  int p_h = 0, p_f = 0;
+  if (edges) {
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < NW; ++w) nit += 5 * s_cnt[w];
+    if constexpr (PF) {
+      if (slot < nit) {
+        item(slot, p_h, p_f);
+        a2_load(p_h, p_f, pf, pg);
+      }
+    }
   }
 
   if (edges && active) {
@@ -501,48 +565,24 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       for (int a = 0; a < NT; ++a) s_tr[((2 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
     }
   }
-  __syncthreads();
-  // phase A2: traces of out-of-block neighbours on the shared edge, one
-  // (neighbour, edge) request per thread instead of a divergent gather inside
-  // the edge loop; same rounding sequence as the owner's phase A
-  int hs[3] = {-1, -1, -1};
   if (edges) {
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int nb = code[j] >> 2;
-        if (code[j] >= 0 && (nb < blo || nb >= bhi)) {
-          const int h = atomicAdd(s_req + HC, 1);
-          if (h < HC) {
-            s_req[h] = code[j];
-            hs[j] = h;
-          }
-        }
-      }
+    // phase A2: traces of out-of-block neighbours on the shared edge (same
+    // rounding sequence as the owner's phase A), instead of divergent
+    // gathers inside the edge loop
+    int it0 = slot;
+    if constexpr (PF) {
+      if (slot < nit) a2_trace(p_h, p_f, pf, pg);
+      it0 += BS;
     }
-    __syncthreads();
-    const int nh = min(s_req[HC], HC);
-    // one (request, field) item per thread
-    for (int it = slot; it < 5 * nh; it += BS) {
-      const int h = it / 5, fi = it - 5 * h;
-      const int cd = s_req[h], nb = cd >> 2, jn = cd & 3;
-      const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
-      double f[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
-      const double nisd = rsqrt(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
-                                     ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
-      const double* L = s_L + jn * K * NT;
-#pragma unroll
-      for (int a = 0; a < NT; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], f[i], acc);
-        s_ht[(fi * NT + a) * HC + h] = __dmul_rn(acc, nisd);
-      }
+    for (int it = it0; it < nit; it += BS) {
+      int hsl, fi;
+      double f[K], g4[4];
+      item(it, hsl, fi);
+      a2_load(hsl, fi, f, g4);
+      a2_trace(hsl, fi, f, g4);
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (!active) return;
 
   double r[3 * K];

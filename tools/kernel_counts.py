@@ -51,8 +51,8 @@ def parse(path, E, stages):
         name = r["Kernel Name"].split("(")[0].replace("void ", "")
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1.0,
-                 "nsecond": 1e-3, "msecond": 1e3}.get(unit, 1.0)
+        scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1.0, "usecond": 1.0,
+                 "ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1.0)
         per[name][r["Metric Name"]] += v * scale
     tot = defaultdict(float)
     for name, m in per.items():
