@@ -69,8 +69,9 @@ typedef struct qf_desc {
   int32_t scn_kind;         /* QF_SCN_* */
   double scn_params[8];
   int32_t has_forcing;      /* momentum forcing + xi mass source of the family */
-  int32_t taylor;           /* MMS: max |2 pi (x_q - x_centroid)| <= 0.06 on this mesh, so the
-                               forcing may use element-local Taylor sin/cos (exact to 1e-19) */
+  int32_t taylor;           /* MMS: 1 if max |2 pi (x_q - x_centroid)| <= 0.06 on this mesh, 2 if
+                               <= 0.02, so the forcing may use element-local Taylor sin/cos of
+                               degree 9 resp. 7 (truncation < 1e-18); 0 = libm sincospi */
   int32_t block;            /* threads per block (0 = default) */
 } qf_desc;
 

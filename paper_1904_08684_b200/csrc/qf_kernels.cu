@@ -647,8 +647,13 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
         if (tay) {
           const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
           double sz, cz, sw, cw;
-          sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-          sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+          if (P.taylor == 2) {
+            sincos_small7(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+            sincos_small7(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+          } else {
+            sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+            sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+          }
           const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
           forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
                       fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),

@@ -310,7 +310,10 @@ class Discretization(HostSetup):
         for i, p in enumerate(scn.device.as_array()):
             d.scn_params[i] = float(p)
         d.has_forcing = 1 if (scn.forcing is not None or scn.mass_source is not None) else 0
-        d.taylor = 1 if self._max_quad_angle() <= 0.06 else 0
+        # element-local Taylor sin/cos for the MMS phases: 1 = degree 9/8
+        # (|z| <= 0.06), 2 = degree 7/6 (|z| <= 0.02); truncation < 1e-18
+        ang = self._max_quad_angle()
+        d.taylor = 2 if ang <= 0.02 else (1 if ang <= 0.06 else 0)
         self._desc = d
         ctx = _cabi.C.c_void_p()
         _cabi.check(lib.qf_create(_cabi.C.byref(d), _cabi.C.byref(ctx)), "qf_create")

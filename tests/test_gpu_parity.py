@@ -288,3 +288,22 @@ def test_walls_conserve_mass_long_run(k):
     m1 = float((sd * out.c[:, 0, 0]).sum())
     assert np.isfinite(out.c).all()
     assert abs(m1 - m0) <= 1e-12 * abs(m0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,level", [(96, 1), (256, 2)])
+def test_mms_taylor_forcing_matches_libm(monkeypatch, n, level):
+    """The element-local Taylor sin/cos of the MMS forcing (degree 9 when
+    max|z| <= 0.06, degree 7 when <= 0.02) agrees with the sincospi path."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import Discretization
+    mesh = M.build_unit_square_mesh(n)
+    scn = S.mms_scenario(dt=2e-5)
+    tay = Discretization(mesh, scn, 2)
+    assert tay._desc.taylor == level
+    monkeypatch.setattr(Discretization, "_max_quad_angle", lambda self: 1.0)
+    lib = Discretization(mesh, scn, 2)
+    assert lib._desc.taylor == 0
+    st = tay.project_initial()
+    a, b = tay.source_rhs(st, 0.37), lib.source_rhs(st, 0.37)
+    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
