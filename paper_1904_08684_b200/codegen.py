@@ -187,11 +187,28 @@ def gen_order(k: int) -> str:
     # ---- U/V rows, input-outer order (volume_kernel, k >= 3): only a, b, wv
     # and the accumulators stay live; cU_i, cV_i, xi_i are fetched once each
     # (the caller pre-scales them by 1/(detB sqrt(detB)) through its view).
-    w("  template <class RT, class CT> static __device__ __forceinline__ void vol_uv_acc(CT cU, CT cV,"
-      " CT xi, const double* a, const double* b, const double* wv,")
+    # outputs [P0, P1) only (the volume kernel splits the output rows across
+    # launches to bound the live accumulators); an input block is emitted only
+    # if one of its outputs is in range (mask), so no dead loads remain
+    def _has(i, p):
+        return any(_nz(rt.T[l, p, i, m]) for l in range(2) for m in range(K))
+    masks = [sum(1 << p for p in range(K) if _has(i, p)) for i in range(K)]
+    cnt = [sum(2 * sum(_nz(rt.T[l, p, i, m]) for l in range(2) for m in range(K)) for i in range(K))
+           for p in range(K)]
+    for G in (2, 3, 4):  # output split points balanced by term count
+        tot, acc, cuts = sum(cnt), 0, [0]
+        for p in range(K):
+            acc += cnt[p]
+            if len(cuts) < G and acc >= tot * len(cuts) / G:
+                cuts.append(p + 1)
+        cuts += [K] * (G + 1 - len(cuts))
+        w(f"  static constexpr int VOL_PSPLIT{G}[{G + 1}] = {{{', '.join(map(str, cuts))}}};")
+    w("  template <int P0 = 0, int P1 = K, class RT, class CT> static __device__ __forceinline__ void"
+      " vol_uv_acc(CT cU, CT cV, CT xi, const double* a, const double* b, const double* wv,")
     w("      double g22, double g21, double g12, double g11, RT rU, RT rV) {")
+    w("    constexpr unsigned R = (1u << P1) - (1u << P0);")
     for i in range(K):
-        w(f"    {{ const double ci = cU[{i}], vi = cV[{i}], xq = xi[{i}];")
+        w(f"    if constexpr (({masks[i]}u & R) != 0u) {{ const double ci = cU[{i}], vi = cV[{i}], xq = xi[{i}];")
         for p in range(K):
             zt = [(rt.T[0, p, i, m], f"a[{m}]") for m in range(K) if _nz(rt.T[0, p, i, m])]
             zt += [(rt.T[1, p, i, m], f"b[{m}]") for m in range(K) if _nz(rt.T[1, p, i, m])]
@@ -199,7 +216,7 @@ def gen_order(k: int) -> str:
             y2 = [(rt.T[1, p, i, m], f"wv[{m}]") for m in range(K) if _nz(rt.T[1, p, i, m])]
             if not (zt or y1 or y2):
                 continue
-            w("      {")
+            w(f"      if constexpr (P0 <= {p} && {p} < P1) {{")
             if zt:
                 w(f"        const double z = {_sum(zt)};")
                 w(f"        rU[{p}] = fma(z, ci, rU[{p}]); rV[{p}] = fma(z, vi, rV[{p}]);")

@@ -345,6 +345,21 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   }
 }
 
+// k >= 3: the U/V rows of the volume contraction are split into VG output
+// groups (term-balanced, Ord<k>::VOL_PSPLIT*), one launch each: fewer live
+// accumulators (no spills) and 1/VG of the literal code per launch
+// (instruction-cache working set); group 0 also writes the xi row
+#ifndef QF_VG4
+#define QF_VG4 2
+#endif
+#ifndef QF_VG3
+#define QF_VG3 1
+#endif
+template <int k>
+struct VGroups {
+  static constexpr int value = k == 4 ? QF_VG4 : (k == 3 ? QF_VG3 : 1);
+};
+
 // orders >= QF_VSPLIT solve the velocity of the new state in its own launch
 #ifndef QF_VSPLIT
 #define QF_VSPLIT 3
@@ -611,6 +626,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
+
   }
   if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725 (+ xi mass source)
     double d1, d2;
@@ -723,7 +739,7 @@ struct GRow {
 #ifndef QF_VOCC
 #define QF_VOCC 1
 #endif
-template <int k>
+template <int k, int GRP = 0>
 __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
                                                      const double* __restrict__ u, int e0, int n,
                                                      double* __restrict__ vol) {
@@ -736,7 +752,7 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
   const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), idet = isd * isd;
   const double i32 = idet * isd, g = P.g;
-  if constexpr (k == 3) {  // measured: the row-outer form is faster at k = 3
+  if constexpr (k == 3 && VGroups<k>::value == 1) {  // measured: row-outer is faster at k = 3
     double cc[3 * K], uu[2 * K], hb[K], r[3 * K];
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
@@ -751,6 +767,12 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     for (int i = 0; i < 3 * K; ++i) vol[i * ld + e] = r[i];
     return;
   }
+  constexpr int VG = VGroups<k>::value, grp = GRP;
+  constexpr int P0 = VG == 1 ? 0 : (VG == 2 ? O::VOL_PSPLIT2[grp] : (VG == 3 ? O::VOL_PSPLIT3[grp]
+                                                                               : O::VOL_PSPLIT4[grp]));
+  constexpr int P1 = VG == 1 ? K : (VG == 2 ? O::VOL_PSPLIT2[grp + 1]
+                                            : (VG == 3 ? O::VOL_PSPLIT3[grp + 1]
+                                                       : O::VOL_PSPLIT4[grp + 1]));
   double r[3 * K], al[K], be[K], wv[K];
   {  // xi row and the U/V operands a, b, w
     double cU[K], cV[K];
@@ -773,9 +795,9 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
       wv[i] = 0.5 * ldg(c + i * ld + e) + (P.hb_linear && i < NH ? ldg(T.hb + i * ld + e) : 0.0);
     }
   }
-  O::vol_uv_acc(GRow{c + K * ld + e, ld, i32}, GRow{c + 2 * K * ld + e, ld, i32},
-                GRow{c + e, ld, i32}, al, be, wv, g * B22, g * B21, g * B12, g * B11, r + K,
-                r + 2 * K);
+  const GRow gU{c + K * ld + e, ld, i32}, gV{c + 2 * K * ld + e, ld, i32}, gX{c + e, ld, i32};
+  O::template vol_uv_acc<P0, P1>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12, g * B11,
+                                 r + K, r + 2 * K);
   if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
     double xi[K], ra[K], rb[K];
 #pragma unroll
@@ -794,13 +816,20 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     }
     O::vol_xi(al, be, rb);
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
+    for (int i = P0; i < P1; ++i) {
       r[K + i] += ghb * ra[i];
       r[2 * K + i] += ghb * rb[i];
     }
   }
+  if constexpr (grp == 0) {
 #pragma unroll
-  for (int i = 0; i < 3 * K; ++i) vol[i * ld + e] = r[i];
+    for (int i = 0; i < K; ++i) vol[i * ld + e] = r[i];
+  }
+#pragma unroll
+  for (int i = P0; i < P1; ++i) {
+    vol[(K + i) * ld + e] = r[K + i];
+    vol[(2 * K + i) * ld + e] = r[2 * K + i];
+  }
 }
 
 template <int k>
@@ -1071,9 +1100,22 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   StageArgs a = a_in;
   if constexpr (k >= 3) {
     if ((a.terms & TERM_VOL) && a.n > 0) {
-      volume_kernel<k><<<(a.n + 127) / 128, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n,
-                                                         x->vol);
+      // one launch per input group (separate register allocation per group)
+      const int vg = (a.n + 127) / 128;
+      volume_kernel<k, 0><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
       g_launches++;
+      if constexpr (VGroups<k>::value > 1) {
+        volume_kernel<k, 1><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+        g_launches++;
+      }
+      if constexpr (VGroups<k>::value > 2) {
+        volume_kernel<k, 2><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+        g_launches++;
+      }
+      if constexpr (VGroups<k>::value > 3) {
+        volume_kernel<k, 3><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+        g_launches++;
+      }
       a.vol = x->vol;
     }
   }
@@ -1329,7 +1371,8 @@ int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* 
 
 static int kernels_per_step(qf_ctx* x) {
   const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
-  return stages * (1 + (x->d.order >= 3) + (x->d.order >= QF_VSPLIT)) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
+  const int vol = x->d.order == 4 ? VGroups<4>::value : (x->d.order == 3 ? VGroups<3>::value : 0);
+  return stages * (1 + vol + (x->d.order >= QF_VSPLIT)) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
 }
 
 int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
