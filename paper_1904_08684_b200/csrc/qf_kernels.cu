@@ -22,6 +22,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <string>
 
@@ -80,6 +81,7 @@ struct StageArgs {
   int e0, n, terms, mode;
   int gstage;                     // Dirichlet ghost table of this stage
   const double* vol;              // k >= 3: precomputed volume rhs [3K][ld] (volume_kernel)
+  int hcap;                       // out-of-block request slots per block (multiple of BS/32)
 };
 
 // ---------------------------------------------------------------- edges
@@ -140,7 +142,7 @@ struct Blk {
 // memory and traced.
 // out-of-block neighbour traces computed cooperatively per block (phase A2)
 #ifndef QF_HCAP
-#define QF_HCAP 64
+#define QF_HCAP 128
 #endif
 // timing experiments only (wrong numerics): in-block traces for every neighbour
 #ifndef QF_FAKE_HALO
@@ -156,7 +158,8 @@ template <int k, int BS = Blk<k>::value>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
-                                          const double* __restrict__ s_ht, int hslot, double B11,
+                                          const double* __restrict__ s_ht, int hslot, int HC,
+                                          double B11,
                                           double B12, double B21, double B22, double isd,
                                           double* r) {
   using O = Ord<k>;
@@ -204,24 +207,38 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
       for (int f = 0; f < 5; ++f)
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          const double v = s_ht[(f * NT + a) * QF_HCAP + (QF_NOFALLBACK ? max(hslot, 0) : hslot)];
+          const double v = s_ht[(f * NT + a) * HC + (QF_NOFALLBACK ? max(hslot, 0) : hslot)];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
     } else {  // request list overflow (rare): gather and trace here, compact code
       const double nisd = rsqrt(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
                                      ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
-      const double* L = s_ht + 5 * NT * QF_HCAP + jn * K * NT;  // s_L (stage_kernel layout)
+      const double* L = s_ht + 5 * NT * HC + jn * K * NT;  // s_L (stage_kernel layout)
 #pragma unroll
       for (int fi = 0; fi < 5; ++fi) {
         const double* src =
             fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+        if constexpr (k <= 2) {  // loads issued together
+          double f[K];
 #pragma unroll
-        for (int a = 0; a < NT; ++a) {
-          double acc = 0.0;
+          for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
+#pragma unroll
+          for (int a = 0; a < NT; ++a) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], f[i], acc);
+            const double v = __dmul_rn(acc, nisd);
+            oth[fi][a] = (a & 1) ? -v : v;  // s -> 1-s
+          }
+        } else {  // rolled (register pressure at high order)
+#pragma unroll
+          for (int a = 0; a < NT; ++a) {
+            double acc = 0.0;
 #pragma unroll 1
-          for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], ldg(src + i * ld + nb), acc);
-          const double v = __dmul_rn(acc, nisd);
-          oth[fi][a] = (a & 1) ? -v : v;  // s -> 1-s
+            for (int i = 0; i < K; ++i) acc = __fma_rn(L[i * NT + a], ldg(src + i * ld + nb), acc);
+            const double v = __dmul_rn(acc, nisd);
+            oth[fi][a] = (a & 1) ? -v : v;  // s -> 1-s
+          }
         }
       }
     }
@@ -434,11 +451,12 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
 
 // ---------------------------------------------------------- stage kernel
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
+// hc: out-of-block request slots per block (runtime, qf_create measures the mesh)
 template <int k>
-constexpr size_t stage_smem_bytes() {
+size_t stage_smem_bytes(int hc) {
   constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
-  return sizeof(double) * (3 * 5 * NT * Blk<k>::value + 5 * NT * QF_HCAP + 3 * K * NT) +
-         sizeof(int) * (QF_HCAP + 8);
+  return sizeof(double) * (3 * 5 * NT * Blk<k>::value + 5 * NT * hc + 3 * K * NT) +
+         sizeof(int) * (hc + 8);
 }
 
 template <int k>
@@ -447,7 +465,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   using O = Ord<k>;
   using TB = Tabs<k>;
   constexpr int K = O::K, NH = O::NH, NQ = O::NQ, NT = O::NT, BS = Blk<k>::value;
-  constexpr int HC = QF_HCAP;
+  const int HC = A.hcap;
   extern __shared__ double smem[];
   double* s_tr = smem;  // trace exchange [3 edges][5 fields][NT][BS]
   double* s_ht = s_tr + 3 * 5 * NT * BS;  // out-of-block neighbour traces [5][NT][HC]
@@ -488,7 +506,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
   // out-of-block neighbour requests, (neighbour, its edge) codes in per-warp
   // slot ranges (ballot prefix, no shared counter); hs[j] = slot or -1
-  constexpr int NW = BS / 32, WC = HC / NW;
+  constexpr int NW = BS / 32;
+  const int WC = HC / NW;
   int* s_cnt = s_req + HC;  // [NW] requests per warp
   int hs[3] = {-1, -1, -1};
   if (edges) {
@@ -694,8 +713,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
     QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < 3; ++j)
-      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], B11, B12, B21, B22,
-                   isd, r);
+      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
+                   B22, isd, r);
   }
   if (A.mode == 0) {
 #pragma unroll
@@ -1055,6 +1074,24 @@ __global__ void fill_kernel(double* buf, size_t n, double v) {
 
 }  // namespace qf
 
+// out-of-block neighbour requests of the busiest warp (blocks of BS slots
+// aligned at slot 0): sizes the stage kernel's request area per mesh
+template <int BS>
+__global__ void request_count_kernel(const int* __restrict__ nbr, int64_t ld, int n,
+                                     int* __restrict__ out) {
+  const int e = blockIdx.x * BS + threadIdx.x;
+  const int blo = blockIdx.x * BS, bhi = min(blo + BS, n);
+  int c = 0;
+  if (e < n) {
+    for (int j = 0; j < 3; ++j) {
+      const int code = nbr[j * ld + e], nb = code >> 2;
+      c += code >= 0 && (nb < blo || nb >= bhi);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, c);
+}
+
 // ===================================================================== ABI
 using namespace qf;
 
@@ -1070,6 +1107,7 @@ struct qf_ctx {
   int graph_launches = 0;
   cudaStream_t stream_hint = nullptr;
   double* vol = nullptr;  // k >= 3 volume-rhs scratch [3K][ld] (context-owned)
+  int hcap = QF_HCAP;     // stage-kernel request slots per block (measured in qf_create)
 };
 
 static thread_local std::string g_last_error;
@@ -1120,10 +1158,12 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
     }
   }
   constexpr int bs = Blk<k>::value;
-  constexpr size_t smem = stage_smem_bytes<k>();
+  a.hcap = x->hcap;
+  const size_t smem = stage_smem_bytes<k>(a.hcap);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(stage_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<k>(QF_HCAP));
     attr = true;
   }
   const int grid = (a.n + bs - 1) / bs;
@@ -1210,6 +1250,28 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
       cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {
     delete x;
     return fail(QF_E_CUDA, "cudaMalloc(error word) failed");
+  }
+  if (d->n_elem > 0) {  // request slots: busiest warp of the mesh, rounded up, capped
+    // (ranges not aligned at slot 0 may overflow into the in-loop gather path)
+    const int bs = d->order <= 1 ? Blk<1>::value : (d->order == 2 ? Blk<2>::value :
+                   (d->order == 3 ? Blk<3>::value : Blk<4>::value));
+    const int nw = bs / 32, grid = (d->n_elem + bs - 1) / bs;
+    int h = 0;
+    cudaMemset(x->err, 0, sizeof(unsigned));
+    if (bs == 128)
+      request_count_kernel<128><<<grid, 128>>>(d->nbr, d->ld, d->n_elem, (int*)x->err);
+    else if (bs == 64)
+      request_count_kernel<64><<<grid, 64>>>(d->nbr, d->ld, d->n_elem, (int*)x->err);
+    else if (bs == 256)
+      request_count_kernel<256><<<grid, 256>>>(d->nbr, d->ld, d->n_elem, (int*)x->err);
+    if (cudaMemcpy(&h, x->err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {
+      cudaFree(x->err);
+      delete x;
+      return fail(QF_E_CUDA, "request count failed");
+    }
+    const int wc = std::min(std::max((h + 3) / 4 * 4, 4), QF_HCAP / nw);
+    x->hcap = wc * nw;
   }
   *out = x;
   return QF_OK;

@@ -143,9 +143,10 @@ class HostSetup:
         ``device_setup`` moves the initial / bathymetry projections to the GPU
         (``qf_project``; default: automatic for large meshes).  ``slot_order``:
         device element slots in Z-order ("locality", default) or mesh order
-        ("natural"; results are identical, only the memory locality differs)."""
-        if slot_order not in ("locality", "natural"):
-            raise ValueError("slot_order must be 'locality' or 'natural'")
+        ("natural") or a seeded shuffle ("random", for tests: every neighbour out
+        of block); results are identical, only the memory locality differs."""
+        if slot_order not in ("locality", "natural", "random"):
+            raise ValueError("slot_order must be 'locality', 'natural' or 'random'")
         self.slot_order = slot_order
         if backend not in ("einsum", "ir"):
             raise ValueError("backend must be 'einsum' or 'ir'")
@@ -181,7 +182,12 @@ class HostSetup:
             self._setup_bathymetry()
         # device slot order: locality (Z-order) permutation of the local rows
         # for a whole mesh; a partition's local order is already sorted
-        self.perm = None if self.partitioned or self.slot_order == "natural" else locality_order(mesh)
+        if self.partitioned or self.slot_order == "natural":
+            self.perm = None
+        elif self.slot_order == "random":
+            self.perm = np.random.default_rng(0).permutation(mesh.n_triangles)
+        else:
+            self.perm = locality_order(mesh)
         slots = self.elements if self.perm is None else self.elements[self.perm]
         self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
                                    slots, self.n_own)
