@@ -148,6 +148,10 @@ struct Blk {
 #ifndef QF_FAKE_HALO
 #define QF_FAKE_HALO 0
 #endif
+// orders whose stage kernel keeps the element's own data in registers
+#ifndef QF_PRE_MAXK
+#define QF_PRE_MAXK 1
+#endif
 #ifndef QF_NOFALLBACK
 #define QF_NOFALLBACK 0
 #endif
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   int code[3] = {0, 0, 0};
   // k <= 2: the element's own data is loaded once up front and stays in
   // registers; for k >= 3 (6K values) each phase re-reads it (L1/L2)
-  constexpr bool PRE = k <= 2;
+  constexpr bool PRE = k <= QF_PRE_MAXK;
   double own_f[PRE ? 6 * K : 1];
   if (edges) {
 #pragma unroll

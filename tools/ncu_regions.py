@@ -23,7 +23,9 @@ def main(rep, order=2):
         if "if (P.forcing)" in l: marks[i] = "forcing"
         if "if (QF_EN_EDGE" in l: marks[i] = "edge loop"
         if "SSP-RK combination" in l: marks[i] = "epilogue"
-        if "phase A" in l: marks[i] = "phase A"
+        if "// phase A: own trace" in l: marks[i] = "phase A"
+        if "// phase A2: traces" in l: marks[i] = "phase A2"
+        if "out-of-block neighbour requests" in l: marks[i] = "requests"
         if "stage_kernel(Tab T" in l: marks[i] = "prologue"
 
     def kregion(ln):
