@@ -150,7 +150,7 @@ struct Blk {
 #endif
 // orders whose stage kernel keeps the element's own data in registers
 #ifndef QF_PRE_MAXK
-#define QF_PRE_MAXK 1
+#define QF_PRE_MAXK 2
 #endif
 #ifndef QF_NOFALLBACK
 #define QF_NOFALLBACK 0
@@ -628,13 +628,14 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
   // own data: still in registers from the prologue when edges are on
   // (u is an operand of the volume terms only, which k >= 3 takes from A.vol)
-  double c[3 * K], u[PRE ? 2 * K : 1], hb[K];
+  double c[3 * K], u[k <= 2 ? 2 * K : 1], hb[K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i)
     c[i] = (PRE && edges) ? own_f[PRE ? i : 0] : ldv(A.c + i * ld + e);
-  if constexpr (PRE) {
+  if constexpr (k <= 2) {
 #pragma unroll
-    for (int i = 0; i < 2 * K; ++i) u[i] = edges ? own_f[3 * K + i] : ldv(A.u + i * ld + e);
+    for (int i = 0; i < 2 * K; ++i)
+      u[i] = (PRE && edges) ? own_f[PRE ? 3 * K + i : 0] : ldv(A.u + i * ld + e);
   }
 #pragma unroll
   for (int i = 0; i < K; ++i)
