@@ -226,7 +226,9 @@ def run_gpu(args):
         os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1904_08684_b200 import distributed as QD
-        return QD.bench_distributed(args, CONFIGS, METRIC)
+        return QD.bench_distributed(args, CONFIGS, METRIC,
+                                    hooks={"clocks": lambda: Clocks(local), "peaks": peaks,
+                                           "alg_bytes": alg_bytes_per_elem})
     lib = _cabi.load()
     k, n, mesh, scn = build_problem(args.config, args.n)
     disc = Discretization(mesh, scn, k)

@@ -220,14 +220,22 @@ class PartitionRunner:
                                  torch.cuda.current_stream().cuda_stream), "qf_rhs")
         return float(lam[:, : self.halo.n_own].max().item())
 
-    def stage(self, si: int, part: str, stream):
-        """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range."""
+    def ghost(self, si: int, stream):
+        """Dirichlet data of stage ``si`` (read by both ranges of the stage)."""
+        d = self.disc
+        if d.tables.bnd_elem.size:
+            self.lib.qf_ghost(d._ctx, self.t + rk_plan(self.k)[si][4] * self.dt, stream.cuda_stream)
+
+    def stage(self, si: int, part: str, stream, ghost: bool = True):
+        """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range
+        (with ``ghost``, the interior / all launch is preceded by the stage's
+        Dirichlet data)."""
         src, dst, a, b, toff = rk_plan(self.k)[si]
         d, lib, h = self.disc, self.lib, self.halo
         s = stream.cuda_stream
         ts = self.t + toff * self.dt
-        if part in ("interior", "all") and d.tables.bnd_elem.size:
-            lib.qf_ghost(d._ctx, ts, s)
+        if ghost and part in ("interior", "all"):
+            self.ghost(si, stream)
         ci, ui = self.bufs[src]
         co, uo = self.bufs[dst]
         e0, n = {"interior": (0, h.n_int), "boundary": (h.n_int, h.n_own - h.n_int),
@@ -266,22 +274,40 @@ class DistributedRunner(PartitionRunner):
             from .solver import cfl_time_step
             self.dt = cfl_time_step(scenario.cfl, order, float(hmin.item()), float(lmax.item()))
         self.comm = torch.cuda.Stream()
+        self.bnd = torch.cuda.Stream()
 
     def step(self):
-        """One SSP-RK step: interior range overlapped with the halo exchange."""
+        """One SSP-RK step.  Per stage: the interior range (no halo
+        dependence) on the main stream, concurrently the cut-adjacent range on
+        its own stream once the stage input's halo has arrived, then the halo
+        exchange of the new cut-adjacent rows on the communication stream,
+        overlapping the next stage's interior range.
+
+        Ordering: boundary(s) waits for the Dirichlet data of stage s and
+        every launch of stage s-1 (event on main) and for exchange(s-1) (comm);
+        interior(s+1) waits for boundary(s); exchange(s) waits for boundary(s).
+        The two ranges of a stage write disjoint rows and read the stage input
+        and the RK base only, the exchange writes halo rows that no interior
+        element reads."""
         torch = self.torch
         main = torch.cuda.current_stream()
         for si in range(len(rk_plan(self.k))):
-            self.stage(si, "interior", main)          # needs no halo
-            main.wait_stream(self.comm)              # halo of the stage input arrived
-            co, uo = self.stage(si, "boundary", main)
-            self.comm.wait_stream(main)
+            self.ghost(si, main)
+            ready = main.record_event()              # stage s-1 complete, ghost data of s
+            self.stage(si, "interior", main, ghost=False)
+            self.bnd.wait_event(ready)
+            self.bnd.wait_stream(self.comm)          # halo of the stage input arrived
+            co, uo = self.stage(si, "boundary", self.bnd, ghost=False)
+            self.comm.wait_stream(self.bnd)
             with torch.cuda.stream(self.comm):
                 self.ex.exchange(co, uo, self.comm)
+            main.wait_stream(self.bnd)               # next stage's interior reads these rows
         self.end_step()
 
     def sync(self):
-        self.torch.cuda.current_stream().wait_stream(self.comm)
+        main = self.torch.cuda.current_stream()
+        main.wait_stream(self.comm)
+        main.wait_stream(self.bnd)
 
 
 class LocalMultiRunner:
@@ -332,8 +358,10 @@ class LocalMultiRunner:
         return out
 
 
-def bench_distributed(args, configs, metric):
-    """Weak scaling: N_rank = N_base^2 elements per GPU, strip partition."""
+def bench_distributed(args, configs, metric, hooks=None):
+    """Weak scaling: N_rank = N_base^2 elements per GPU, strip partition.
+    ``hooks`` (from bench.py): ``clocks()`` -> NVML sampler, ``peaks()`` ->
+    (HBM GB/s, source), ``alg_bytes(K, r)`` -> algorithmic bytes per element."""
     import json
 
     import torch
@@ -358,6 +386,7 @@ def bench_distributed(args, configs, metric):
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
     n_launch0 = run.lib.qf_launch_count()
     main = torch.cuda.current_stream()
+    clocks = hooks["clocks"]() if hooks else None
     total = 0.0
     for it in range(args.steps):
         flush.fill_(float(it))  # outside the timed events
@@ -366,9 +395,12 @@ def bench_distributed(args, configs, metric):
         run.step()
         run.sync()
         e1.record(main)
+        if clocks is not None:
+            clocks.sample()
         torch.cuda.synchronize()
         total += e0.elapsed_time(e1)
     launches = run.lib.qf_launch_count() - n_launch0
+    clk = clocks.stop() if clocks is not None else None
     # e2e: owned state H2D from pinned host memory + step + D2H of (c, u), per step
     nown, ldl = run.halo.n_own, run.ld
     host_c = torch.empty((3 * run.K, nown), dtype=torch.float64).pin_memory()
@@ -409,8 +441,18 @@ def bench_distributed(args, configs, metric):
                         "h2d_bytes_per_step": 8 * 3 * K * mesh.n_triangles,
                         "d2h_bytes_per_step": 8 * 5 * K * mesh.n_triangles,
                         "timing": "per-rank owned-state H2D + step + D2H, CUDA events, max over ranks"},
-                "roofline": {"bound": "hbm", "unit": "GB/s", "peak": None, "achieved": None,
-                             "frac": None, "traffic": None,
-                             "note": "per-kernel roofline is reported by the N=1 line"}}
+                "clocks": clk}
+        if hooks:
+            # per GPU: algorithmic bytes of the largest rank's owned elements
+            # per step over the step time (halo exchange included)
+            peak, src = hooks["peaks"]()
+            rvec = [0] + [1] * (ns - 1)
+            e_rank = int(np.bincount(part, minlength=world).max())
+            by = sum(e_rank * hooks["alg_bytes"](K, r) for r in rvec)
+            ach = by / (t_ms / args.steps * 1e-3) / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                "frac": ach / peak, "traffic": None, "peak_source": src,
+                                "kernel": "whole step per GPU (stage launches + halo exchange)",
+                                "note": "ncu traffic and FP64 fraction: see the N=1 line"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
