@@ -58,6 +58,19 @@ __device__ __forceinline__ void sincos_small(double z, double& s, double& c) {
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
+// 1/sqrt(x) for normal positive x: MUFU seed (rsqrt.approx.f64) + one
+// third-order Newton step; <= 1.21 ulp, x * rsqrt_fast(x) <= 0.99 ulp from
+// sqrt(x) (tools/micro/rsqrt_acc.cu).  ~6 instructions instead of the
+// library's ~20 with special-case branches; used by every kernel for detB,
+// edge normals and wave speeds, so all threads that evaluate the same
+// quantity get the same bits.
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);  // 1 - x y^2
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
 // ------------------------------------------------------------ scenarios
 // Closed forms of paper_1904_08684_b200/scenario.py (reference
 // scenario.py:51-55 exact_with_velocity, :69-94 manufactured forcing).

@@ -173,7 +173,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
   const double d2 = j == 0 ? 1.0 : (j == 1 ? -1.0 : 0.0);
   const double dx = B11 * d1 + B12 * d2, dy = B21 * d1 + B22 * d2;
-  const double l2 = dx * dx + dy * dy, il = rsqrt(l2);
+  const double l2 = dx * dx + dy * dy, il = rsqrt_fast(l2);
   const double n1 = dy * il, n2 = -dx * il;
 
   double own[6][NT], oth[6][NT];
@@ -215,7 +215,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
     } else {  // request list overflow (rare): gather and trace here, compact code
-      const double nisd = rsqrt(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
+      const double nisd = rsqrt_fast(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
                                      ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
       const double* L = s_ht + 5 * NT * HC + jn * K * NT;  // s_L (stage_kernel layout)
 #pragma unroll
@@ -292,10 +292,10 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     unN[a] = n1 * oth[3][a] + n2 * oth[4][a];
     tmp[a] = own[5][a] + own[0][a];
   }
-  // sqrt(max(gH, 0)) as x * rsqrt(x): ~1 ulp, identical on both sides of an edge
+  // sqrt(max(gH, 0)) as x * rsqrt_fast(x): ~1 ulp, identical on both sides of an edge
   auto wave = [&](double H) {
     const double x = P.g * H;
-    return x > 0.0 ? x * rsqrt(x) : 0.0;
+    return x > 0.0 ? x * rsqrt_fast(x) : 0.0;
   };
   double lam = 0.0, hmin = 1.0;
   O::samples(tmp, sH);
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   }
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
-  const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), sd = det * isd, idet = isd * isd;
+  const double det = det2(B11, B12, B21, B22), isd = rsqrt_fast(det), sd = det * isd, idet = isd * isd;
   // out-of-block neighbour requests, (neighbour, its edge) codes in per-warp
   // slot ranges (ballot prefix, no shared counter); hs[j] = slot or -1
   constexpr int NW = BS / 32;
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   };
   auto a2_trace = [&](int hsl, int fi, const double* f, const double* g4) {
     const int cd = s_req[hsl], jn = cd & 3;
-    const double nisd = rsqrt(det2(g4[0], g4[1], g4[2], g4[3]));
+    const double nisd = rsqrt_fast(det2(g4[0], g4[1], g4[2], g4[3]));
     const double* L = s_L + jn * K * NT;
 #pragma unroll
     for (int a = 0; a < NT; ++a) {
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
   const int64_t ld = T.ld;
   const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
   const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
-  const double det = det2(B11, B12, B21, B22), isd = rsqrt(det), idet = isd * isd;
+  const double det = det2(B11, B12, B21, B22), isd = rsqrt_fast(det), idet = isd * isd;
   const double i32 = idet * isd, g = P.g;
   if constexpr (k == 3 && VGroups<k>::value == 1) {  // measured: row-outer is faster at k = 3
     double cc[3 * K], uu[2 * K], hb[K], r[3 * K];
@@ -1021,7 +1021,7 @@ __global__ void static_kernel(Tab T, int n, double* __restrict__ hbt) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const int64_t ld = T.ld;
-  const double isd = rsqrt(det2(T.geo[e], T.geo[ld + e], T.geo[2 * ld + e], T.geo[3 * ld + e]));
+  const double isd = rsqrt_fast(det2(T.geo[e], T.geo[ld + e], T.geo[2 * ld + e], T.geo[3 * ld + e]));
   double f[K], t3[NT];
 #pragma unroll
   for (int i = 0; i < K; ++i) f[i] = i < NH ? T.hb[i * ld + e] : 0.0;
