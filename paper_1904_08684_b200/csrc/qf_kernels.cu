@@ -302,8 +302,9 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   O::samples(unO, sU);
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    lam = fmax(lam, fabs(sU[s]) + wave(sH[s]));
-    hmin = fmin(hmin, sH[s]);
+    const double w = fabs(sU[s]) + wave(sH[s]);
+    lam = w > lam ? w : lam;  // (plain selects: fmax/fmin carry NaN handling)
+    hmin = sH[s] < hmin ? sH[s] : hmin;
   }
   if (dirichlet) {
 #pragma unroll
@@ -319,8 +320,9 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   }
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    lam = fmax(lam, fabs(sU[s]) + wave(sH[s]));
-    hmin = fmin(hmin, sH[s]);
+    const double w = fabs(sU[s]) + wave(sH[s]);
+    lam = w > lam ? w : lam;  // (plain selects: fmax/fmin carry NaN handling)
+    hmin = sH[s] < hmin ? sH[s] : hmin;
   }
   if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
   if (A.lam) A.lam[j * ld + e] = lam;
