@@ -138,6 +138,16 @@ int qf_gather(const double* src, int64_t ld_src, const int32_t* idx, int32_t n_i
 int qf_scatter(const double* src, const int32_t* idx, int32_t n_idx, int32_t rows,
                double* dst, int64_t ld_dst, void* stream);
 
+/* harness.l2_error (harness.py:81-98) on the device: sq[0..2] (DEVICE, 3
+ * doubles) = squared global L2 errors of xi, U, V of state c against the
+ * scenario's exact solution at time t over elements [e0, e0+n) (n < 0: all
+ * owned), at the degree-(2k+2) collapsed Gauss rule; deterministic
+ * reduction order.  QF_E_ARG if the scenario family has no device exact
+ * solution (QF_SCN_NONE).  The L2 norms are sqrt(sq) (after an allreduce-sum
+ * over partitions). */
+int qf_l2_error(qf_ctx* ctx, const double* c, double t, int32_t e0, int32_t n, double* sq,
+                void* stream);
+
 /* Read (and optionally clear) the error word; synchronises `stream`. */
 int qf_error(qf_ctx* ctx, uint32_t* bits, int32_t clear, void* stream);
 

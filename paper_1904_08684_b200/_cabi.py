@@ -21,7 +21,7 @@ TERM_VOLUME, TERM_EDGE, TERM_SOURCE, TERM_ALL = 1, 2, 4, 7
 
 EXPORTS = (
     "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
-    "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill",
+    "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error",
     "qf_launch_count", "qf_last_error", "qf_abi_version",
 )
 
@@ -68,6 +68,7 @@ def load(path: Path | None = None):
         "qf_scatter": (C.c_int, [vp, vp, i32, i32, vp, i64, vp]),
         "qf_error": (C.c_int, [vp, C.POINTER(C.c_uint32), i32, vp]),
         "qf_fill": (C.c_int, [vp, C.c_size_t, d, vp]),
+        "qf_l2_error": (C.c_int, [vp, vp, d, i32, i32, vp, vp]),
         "qf_launch_count": (C.c_uint64, []),
         "qf_last_error": (C.c_char_p, []),
         "qf_abi_version": (C.c_int, []),

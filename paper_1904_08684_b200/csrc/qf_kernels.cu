@@ -158,14 +158,15 @@ struct Blk {
 #ifndef QF_FAKE_HBT
 #define QF_FAKE_HBT 0
 #endif
+// Lax-Friedrichs flux moments F[3][NT] of local edge j of element e and the
+// lift scale s = edge length / sqrt(detB) (reference solver.py:561-688).
 template <int k, int BS = Blk<k>::value>
-__device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
+__device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
                                           const double* __restrict__ s_ht, int hslot, int HC,
-                                          double B11,
-                                          double B12, double B21, double B22, double isd,
-                                          double* r) {
+                                          double B11, double B12, double B21, double B22,
+                                          double isd, double (&F)[3][Ord<k>::NT], double& s) {
   using O = Ord<k>;
   constexpr int K = O::K, NT = O::NT, NH = O::NH;
   const int64_t ld = T.ld;
@@ -340,7 +341,6 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   O::jprod(oth[1], unN, aN);
   O::jprod(own[2], unO, bO);
   O::jprod(oth[2], unN, bN);
-  double F[3][NT];
   const double hl = 0.5 * lam, g = P.g;
 #pragma unroll
   for (int a = 0; a < NT; ++a) {
@@ -351,8 +351,23 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     F[1][a] = 0.5 * (aO[a] + aN[a] + g * n1 * pr) + hl * (own[1][a] - oth[1][a]);
     F[2][a] = 0.5 * (bO[a] + bN[a] + g * n2 * pr) + hl * (own[2][a] - oth[2][a]);
   }
+  s = l2 * il * isd;  // edge length / sqrt(detB)
+}
+
+template <int k, int BS = Blk<k>::value>
+__device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
+                                          int j, int code, int slot, int blo, int bhi,
+                                          const double* __restrict__ s_tr,
+                                          const double* __restrict__ s_ht, int hslot, int HC,
+                                          double B11,
+                                          double B12, double B21, double B22, double isd,
+                                          double* r) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NT = O::NT;
+  double F[3][NT], s;
+  edge_flux<k, BS>(T, P, A, e, j, code, slot, blo, bhi, s_tr, s_ht, hslot, HC, B11, B12, B21, B22,
+                   isd, F, s);
   // lift: r_f[p] -= (len / sqrt(detB)) sum_a Lambda_j[p, a] F_f[a]
-  const double s = l2 * il * isd;  // edge length / sqrt(detB)
   if (j == 0) {
     O::lift0(F[0], s, r);
     O::lift0(F[1], s, r + K);
@@ -452,6 +467,59 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
       r[K + i] += ghb * ra[i];
       r[2 * K + i] += ghb * rb[i];
     }
+  }
+}
+
+// Manufactured forcing at the (k+2)^2 collapsed Gauss points of element e
+// (reference solver.py:719-724, scenario.py:78-93): sink(P_q, S, Fx, Fy)
+// with P_q[p] = w_q phi_p(q) and the point values already scaled by sqrt(detB).
+template <int k, class Sink>
+__device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e, double t,
+                                             double B11, double B12, double B21, double B22,
+                                             double sd, Sink&& sink) {
+  using TB = Tabs<k>;
+  constexpr int K = Ord<k>::K, NQ = Ord<k>::NQ;
+  const int64_t ld = T.ld;
+  const double* s_tab = TB::ptr();
+  const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
+  double st, ct;
+  sincospi(2.0 * t, &st, &ct);
+  // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
+  // value by a Taylor-evaluated small angle (2 sincospi per element
+  // instead of 2 per quadrature point)
+  const bool tay = P.kind == SCN_MMS && P.taylor;
+  // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
+  // the centroid; per point only small-angle Taylor rotations follow
+  const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
+  double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
+  if (tay) {
+    sincospi(2.0 * (x0 - t), &sx0, &cx0);
+    sincospi(2.0 * (y0 - t), &sy0, &cy0);
+    sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
+  }
+  QF_UNROLL(QF_QUNROLL)
+  for (int q = 0; q < NQ; ++q) {
+    const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
+    const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+    double S, Fx, Fy;
+    if (tay) {
+      const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
+      double sz, cz, sw, cw;
+      if (P.taylor == 2) {
+        sincos_small7(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+        sincos_small7(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+      } else {
+        sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
+        sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+      }
+      const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
+      forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
+                  fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
+                  fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
+    } else {
+      forcing(P, x, y, t, st, ct, S, Fx, Fy);
+    }
+    sink(s_tab + TB::P + q * K, S * sd, Fx * sd, Fy * sd);
   }
 }
 
@@ -665,56 +733,16 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
     }
     if (P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
-      const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
-      double st, ct;
-      sincospi(2.0 * t, &st, &ct);
-      // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
-      // value by a Taylor-evaluated small angle (2 sincospi per element
-      // instead of 2 per quadrature point)
-      const bool tay = P.kind == SCN_MMS && P.taylor;
-      // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
-      // the centroid; per point only small-angle Taylor rotations follow
-      const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
-      double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
-      if (tay) {
-        sincospi(2.0 * (x0 - t), &sx0, &cx0);
-        sincospi(2.0 * (y0 - t), &sy0, &cy0);
-        sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
-      }
-      QF_UNROLL(QF_QUNROLL)
-      for (int q = 0; q < NQ; ++q) {
-        const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
-        const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
-        double S, Fx, Fy;
-        if (tay) {
-          const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
-          double sz, cz, sw, cw;
-          if (P.taylor == 2) {
-            sincos_small7(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-            sincos_small7(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
-          } else {
-            sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-            sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
-          }
-          const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
-          forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
-                      fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
-                      fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
-        } else {
-          forcing(P, x, y, t, st, ct, S, Fx, Fy);
-        }
-        S *= sd;
-        Fx *= sd;
-        Fy *= sd;
-        const double* Pq = s_tab + TB::P + q * K;
+      forcing_quad<k>(P, T, e, t, B11, B12, B21, B22, sd,
+                      [&](const double* Pq, double S, double Fx, double Fy) {
 #pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const double w = Pq[p];
-          r[p] = fma(w, S, r[p]);
-          r[K + p] = fma(w, Fx, r[K + p]);
-          r[2 * K + p] = fma(w, Fy, r[2 * K + p]);
-        }
-      }
+                        for (int p = 0; p < K; ++p) {
+                          const double w = Pq[p];
+                          r[p] = fma(w, S, r[p]);
+                          r[K + p] = fma(w, Fx, r[K + p]);
+                          r[2 * K + p] = fma(w, Fy, r[2 * K + p]);
+                        }
+                      });
     }
   }
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
@@ -1039,6 +1067,93 @@ __global__ void static_kernel(Tab T, int n, double* __restrict__ hbt) {
   hbt[3 * NT * ld + e] = __dmul_rn(__dmul_rn(f[0], isd), 0.7071067811865476);
 }
 
+// Global L2 error against the scenario's exact solution (reference
+// harness.py:81-98): per element
+//   detB * sum_q w_q ((sum_p c[f][p] phi_p(q)) / sqrt(detB) - exact_f(x_q, t))^2
+// for f = xi, U, V at the degree-(2k+2) collapsed rule; block sums in a fixed
+// tree order, then one block adds the partials in block order, so the result
+// is deterministic (independent of scheduling).
+constexpr int L2_BS = 256;
+
+template <int k>
+__global__ void __launch_bounds__(L2_BS)
+    l2err_kernel(Tab T, Phys P, const double* __restrict__ c, int e0, int n, double t,
+                 double* __restrict__ part) {
+  using O = Ord<k>;
+  using TB = Tabs<k>;
+  constexpr int K = O::K, NQ = O::NQ;
+  __shared__ double s[3][L2_BS];
+  const int tid = threadIdx.x, e = e0 + blockIdx.x * L2_BS + tid;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (e < e0 + n) {
+    const int64_t ld = T.ld;
+    const double B11 = T.geo[e], B12 = T.geo[ld + e], B21 = T.geo[2 * ld + e],
+                 B22 = T.geo[3 * ld + e];
+    const double a1x = T.geo[4 * ld + e], a1y = T.geo[5 * ld + e];
+    const double det = det2(B11, B12, B21, B22), sd = sqrt(det);
+    double cc[3 * K];
+#pragma unroll
+    for (int i = 0; i < 3 * K; ++i) cc[i] = c[i * ld + e];
+    const double* tab = TB::ptr();
+    for (int q = 0; q < NQ; ++q) {
+      const double x1 = tab[TB::QX + q], x2 = tab[TB::QY + q];
+      const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+      double ex[3];
+      exact3(P, x, y, t, ex[0], ex[1], ex[2]);
+      const double w = tab[TB::QW + q];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        double v = 0.0;
+#pragma unroll
+        for (int p = 0; p < K; ++p) v = fma(cc[f * K + p], tab[TB::PHI + q * K + p], v);
+        const double d = v / sd - ex[f];
+        acc[f] = fma(w, d * d, acc[f]);
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < 3; ++f) acc[f] *= det;
+  }
+#pragma unroll
+  for (int f = 0; f < 3; ++f) s[f][tid] = acc[f];
+  __syncthreads();
+  for (int h = L2_BS / 2; h > 0; h >>= 1) {
+    if (tid < h) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) s[f][tid] += s[f][tid + h];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) part[(int64_t)f * gridDim.x + blockIdx.x] = s[f][0];
+  }
+}
+
+// sq[f] = sum over nb block partials (fixed order: strided per thread, tree)
+__global__ void __launch_bounds__(L2_BS) l2sum_kernel(const double* __restrict__ part, int nb,
+                                                      double* __restrict__ sq) {
+  __shared__ double s[3][L2_BS];
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double a = 0.0;
+    for (int b = tid; b < nb; b += L2_BS) a += part[(int64_t)f * nb + b];
+    s[f][tid] = a;
+  }
+  __syncthreads();
+  for (int h = L2_BS / 2; h > 0; h >>= 1) {
+    if (tid < h) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) s[f][tid] += s[f][tid + h];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) sq[f] = s[f][0];
+  }
+}
+
 __global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
 
 __global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
@@ -1115,6 +1230,8 @@ struct qf_ctx {
   cudaStream_t stream_hint = nullptr;
   double* vol = nullptr;  // k >= 3 volume-rhs scratch [3K][ld] (context-owned)
   int hcap = QF_HCAP;     // stage-kernel request slots per block (measured in qf_create)
+  double* l2part = nullptr;  // qf_l2_error block partials [3][blocks] (grown on demand)
+  int l2cap = 0;
 };
 
 static thread_local std::string g_last_error;
@@ -1222,6 +1339,14 @@ static void launch_project(qf_ctx* x, const double* prog, int n, double h_min, d
   g_launches++;
 }
 
+template <int k>
+static void launch_l2(qf_ctx* x, const double* c, double t, int e0, int n, int nb, double* sq,
+                      cudaStream_t s) {
+  l2err_kernel<k><<<nb, L2_BS, 0, s>>>(x->tab, x->phys, c, e0, n, t, x->l2part);
+  l2sum_kernel<<<1, L2_BS, 0, s>>>(x->l2part, nb, sq);
+  g_launches += 2;
+}
+
 extern "C" {
 
 int qf_abi_version(void) { return 1; }
@@ -1288,6 +1413,7 @@ void qf_destroy(qf_ctx* x) {
   if (!x) return;
   if (x->graph) cudaGraphExecDestroy(x->graph);
   if (x->vol) cudaFree(x->vol);
+  if (x->l2part) cudaFree(x->l2part);
   cudaFree(x->err);
   delete x;
 }
@@ -1315,6 +1441,27 @@ int qf_project(qf_ctx* x, const double* prog, int32_t n, double h_min, double* c
   QF_DISPATCH(x->d.order, launch_project, x, prog, n, h_min, c, hb);
   QF_DISPATCH(x->d.order, launch_static, x, n, (cudaStream_t)stream);
   return cuda_check("project_kernel");
+}
+
+int qf_l2_error(qf_ctx* x, const double* c, double t, int32_t e0, int32_t n, double* sq,
+                void* stream) {
+  if (!x || !c || !sq) return fail(QF_E_ARG, "null argument");
+  if (x->phys.kind == SCN_NONE) return fail(QF_E_ARG, "scenario has no device exact solution");
+  if (n < 0) {
+    e0 = 0;
+    n = x->d.n_elem;
+  }
+  const int nb = std::max((n + L2_BS - 1) / L2_BS, 1);
+  if (nb > x->l2cap) {
+    if (x->l2part) cudaFree(x->l2part);
+    x->l2part = nullptr;
+    x->l2cap = 0;
+    if (cudaMalloc(&x->l2part, sizeof(double) * 3 * (size_t)nb) != cudaSuccess)
+      return fail(QF_E_CUDA, "cudaMalloc(l2 partials) failed");
+    x->l2cap = nb;
+  }
+  QF_DISPATCH(x->d.order, launch_l2, x, c, t, e0, n, nb, sq, (cudaStream_t)stream);
+  return cuda_check("l2err_kernel");
 }
 
 int qf_ghost(qf_ctx* x, double t, void* stream) {

@@ -557,6 +557,16 @@ class Discretization(HostSetup):
             self._cfl_warned = True
 
     # ------------------------------------------------------ time stepping
+    def l2_error_sq(self, state, t: float) -> np.ndarray:
+        """Squared L2 errors (xi, U, V) of the owned elements against the
+        scenario's exact solution at t, evaluated on the device (qf_l2_error;
+        reference harness.py:81-98).  ``state``: State or DeviceState."""
+        ds = state if isinstance(state, DeviceState) else self.to_device(state, solve=False)
+        sq = self.torch.zeros(3, dtype=self.torch.float64, device=self.device)
+        self._check(self._lib.qf_l2_error(self._ctx, ds.c.data_ptr(), float(t), 0, self.n_own,
+                                          sq.data_ptr(), self._stream), "qf_l2_error")
+        return sq.cpu().numpy()
+
     def _work_buf(self):
         if self._work is None:
             self._work = self.torch.empty(2 * 5 * self.K * self.ld, dtype=self.torch.float64,

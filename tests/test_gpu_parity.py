@@ -309,3 +309,46 @@ def test_mms_taylor_forcing_matches_libm(monkeypatch, n, level):
     st = tay.project_initial()
     a, b = tay.source_rhs(st, 0.37), lib.source_rhs(st, 0.37)
     assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("k,n,steps", [(0, 8, 3), (1, 16, 20), (2, 16, 20), (3, 8, 10), (4, 6, 5)])
+def test_l2_error_device_matches_host(k, n, steps):
+    """qf_l2_error (device quadrature + deterministic reduction) == the
+    reference's host l2_error form (harness.py:81-98) on the same state, and
+    partition sums of squares add up to the single-domain value."""
+    from paper_1904_08684_b200 import harness as Hn, mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import Discretization
+    scn = S.mms_scenario(dt=1e-4)
+    mesh = M.build_unit_square_mesh(n)
+    disc = Discretization(mesh, scn, k)
+    st = disc.run(disc.project_initial(), t_end=steps * 1e-4)
+    t = st.t
+    dev = Hn.l2_error(disc, st, t, device=True)
+    again = Hn.l2_error(disc, st, t, device=True)
+    assert dev.errors() == again.errors()  # deterministic
+    host = Hn.l2_error(disc, st, t, device=False)
+    # errors ~1e-6 of O(1) fields: roundoff of c_h(x_q) - exact is amplified
+    # ~1e6-fold, so 1e-9 relative (the tolerance of the reference sweep pins)
+    assert np.allclose(dev.errors(), host.errors(), rtol=1e-9, atol=0)
+    # partitioned: owned elements of 2 strips, sum of squares
+    from paper_1904_08684_b200.distributed import strip_partition, build_halo
+    part = strip_partition(n, 2)
+    tot = np.zeros(3)
+    for r in range(2):
+        h = build_halo(mesh, part, r)
+        d = Discretization(mesh, scn, k, elements=h.elements, n_own=h.n_own)
+        c = st.c[h.elements]
+        from paper_1904_08684_b200.solver import DeviceState
+        cd = d.upload_fields(c)
+        tot += d.l2_error_sq(DeviceState(cd, None, None), t)
+    assert np.allclose(np.sqrt(tot), dev.errors(), rtol=1e-12, atol=0)
+
+
+def test_l2_error_device_rejects_no_exact():
+    """Scenario families without a device exact solution: QF_E_ARG."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import Discretization
+    disc = Discretization(M.build_unit_square_mesh(8), S.bump_scenario(), 2)
+    st = disc.project_initial()
+    with pytest.raises(RuntimeError):
+        disc.l2_error_sq(st, 0.0)

@@ -256,7 +256,7 @@ def test_codegen_deterministic_and_current():
 def test_cabi_exports_every_header_symbol():
     from paper_1904_08684_b200 import _cabi
     hdr = open(os.path.join(ROOT, "include", "qfswe.h")).read()
-    names = set(re.findall(r"\b(qf_[a-z_]+)\s*\(", hdr))
+    names = set(re.findall(r"\b(qf_[a-z0-9_]+)\s*\(", hdr))
     assert names == set(_cabi.EXPORTS)
     lib = _cabi.load()
     for n in names:
