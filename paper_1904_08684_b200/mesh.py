@@ -449,6 +449,19 @@ def locality_order(mesh: Mesh, elements=None) -> np.ndarray:
         return np.zeros(0, dtype=np.int64)
     cen = mesh.vertices[mesh.triangles[el]].mean(axis=1)
     lo, hi = cen.min(axis=0), cen.max(axis=0)
-    q = ((cen - lo) / np.maximum(hi - lo, 1e-300) * 65535.0).astype(np.int64)
+    # lattice of the element size (sqrt of twice the mean area: the quad
+    # side of a split-square mesh, whose two triangles then share a cell), so
+    # that aligned Morton blocks are whole square patches for any N, not
+    # only powers of two (N = 1448: 28 -> 54 out-of-block edges per
+    # 128-element block with the range-scaled lattice)
+    v = mesh.vertices[mesh.triangles[el]]
+    area = 0.5 * np.abs((v[:, 1, 0] - v[:, 0, 0]) * (v[:, 2, 1] - v[:, 0, 1])
+                        - (v[:, 2, 0] - v[:, 0, 0]) * (v[:, 1, 1] - v[:, 0, 1]))
+    h = float(np.sqrt(2.0 * area.mean()))
+    span = float((hi - lo).max())
+    if h > 0.0 and span / h < 65535.0:
+        q = np.floor((cen - lo) / h + 1.0 / 6.0).astype(np.int64)
+    else:
+        q = ((cen - lo) / np.maximum(hi - lo, 1e-300) * 65535.0).astype(np.int64)
     code = _spread16(q[:, 0]) | (_spread16(q[:, 1]) << np.uint64(1))
     return np.argsort(code, kind="stable")
