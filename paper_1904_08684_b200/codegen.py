@@ -155,8 +155,8 @@ def gen_order(k: int) -> str:
         w(f"    r[{p}] = {_sum(terms)};")
     w("  }")
     # ---- U/V rows
-    w("  template <class RT, class CT> static __device__ __forceinline__ void vol_uv(CT cU, CT cV,"
-      " CT xi, const double* a, const double* b, const double* wv,")
+    w("  template <bool PRESS = true, class RT, class CT> static __device__ __forceinline__ void"
+      " vol_uv(CT cU, CT cV, CT xi, const double* a, const double* b, const double* wv,")
     w("      double g22, double g21, double g12, double g11, RT rU, RT rV) {")
     for p in range(K):
         w(f"    {{ double su = 0.0, sv = 0.0;")
@@ -171,6 +171,8 @@ def gen_order(k: int) -> str:
             if zt:
                 w(f"        const double z = {_sum(zt)};")
                 w(f"        su = fma(z, cU[{i}], su); sv = fma(z, cV[{i}], sv);")
+            if y1 or y2:
+                w("        if constexpr (PRESS) {")
             if y1 and y2:
                 w(f"        const double y1 = {_sum(y1)}, y2 = {_sum(y2)};")
                 w(f"        su = fma(xi[{i}], fma(g22, y1, -g21 * y2), su);")
@@ -181,6 +183,8 @@ def gen_order(k: int) -> str:
             elif y2:
                 w(f"        const double y2 = {_sum(y2)};")
                 w(f"        su = fma(-xi[{i}] * g21, y2, su); sv = fma(xi[{i}] * g11, y2, sv);")
+            if y1 or y2:
+                w("        }")
             w("      }")
         w(f"      rU[{p}] = su; rV[{p}] = sv; }}")
     w("  }")
@@ -203,8 +207,9 @@ def gen_order(k: int) -> str:
                 cuts.append(p + 1)
         cuts += [K] * (G + 1 - len(cuts))
         w(f"  static constexpr int VOL_PSPLIT{G}[{G + 1}] = {{{', '.join(map(str, cuts))}}};")
-    w("  template <int P0 = 0, int P1 = K, class RT, class CT> static __device__ __forceinline__ void"
-      " vol_uv_acc(CT cU, CT cV, CT xi, const double* a, const double* b, const double* wv,")
+    w("  template <int P0 = 0, int P1 = K, bool PRESS = true, class RT, class CT> static __device__"
+      " __forceinline__ void vol_uv_acc(CT cU, CT cV, CT xi, const double* a, const double* b,"
+      " const double* wv,")
     w("      double g22, double g21, double g12, double g11, RT rU, RT rV) {")
     w("    constexpr unsigned R = (1u << P1) - (1u << P0);")
     for i in range(K):
@@ -220,6 +225,8 @@ def gen_order(k: int) -> str:
             if zt:
                 w(f"        const double z = {_sum(zt)};")
                 w(f"        rU[{p}] = fma(z, ci, rU[{p}]); rV[{p}] = fma(z, vi, rV[{p}]);")
+            if y1 or y2:
+                w("        if constexpr (PRESS) {")
             if y1 and y2:
                 w(f"        const double y1 = {_sum(y1)}, y2 = {_sum(y2)};")
                 w(f"        rU[{p}] = fma(xq, fma(g22, y1, -g21 * y2), rU[{p}]);")
@@ -230,8 +237,53 @@ def gen_order(k: int) -> str:
             elif y2:
                 w(f"        const double y2 = {_sum(y2)};")
                 w(f"        rU[{p}] = fma(-xq * g21, y2, rU[{p}]); rV[{p}] = fma(xq * g11, y2, rV[{p}]);")
+            if y1 or y2:
+                w("        }")
             w("      }")
         w("    }")
+    w("  }")
+    # ---- pressure rows from the symmetric products (k >= 3 volume): with
+    # T_l[p, i, m] symmetric in (i, m),
+    #   pi_l[p] = T_l : (xi (x) (xi / 2 + hb))
+    #           = sum_{i<m} T_l[p,i,m] xi_i xi_m + 1/2 sum_i T_l[p,i,i] xi_i^2
+    #             + sum_{i, m<NH} T_l[p,i,m] xi_i hb_m
+    # (about half the multiply-adds of the y_l = T_l w contraction), then
+    # U_p += g22 pi_1 - g21 pi_2, V_p += g11 pi_2 - g12 pi_1 (rows [P0, P1))
+    w("  template <int P0 = 0, int P1 = K, class RT> static __device__ __forceinline__ void"
+      " vol_press(const double* xi, const double* hb, bool hbl, double g22, double g21,"
+      " double g12, double g11, RT rU, RT rV) {")
+    w("    constexpr unsigned R = (1u << P1) - (1u << P0);")
+    w("    double p1[K], p2[K];")
+    w("    #pragma unroll\n    for (int p = 0; p < K; ++p) { p1[p] = 0.0; p2[p] = 0.0; }")
+
+    def _press_block(pairs, xa, xb, half_diag):
+        for (i, m) in pairs:
+            ent = []
+            for p in range(K):
+                f = 0.5 if (half_diag and i == m) else 1.0
+                c1, c2 = f * rt.T[0, p, i, m], f * rt.T[1, p, i, m]
+                if _nz(c1) or _nz(c2):
+                    ent.append((p, c1, c2))
+            if not ent:
+                continue
+            mask = sum(1 << p for p, _, _ in ent)
+            w(f"    if constexpr (({mask}u & R) != 0u) {{ const double q = {xa}[{i}] * {xb}[{m}];")
+            for p, c1, c2 in ent:
+                st = []
+                if _nz(c1):
+                    st.append(f"p1[{p}] = fma({scoef(c1)}, q, p1[{p}]);")
+                if _nz(c2):
+                    st.append(f"p2[{p}] = fma({scoef(c2)}, q, p2[{p}]);")
+                w(f"      if constexpr (P0 <= {p} && {p} < P1) {{ {' '.join(st)} }}")
+            w("    }")
+
+    _press_block([(i, m) for i in range(K) for m in range(i, K)], "xi", "xi", True)
+    w("    if (hbl) {")
+    _press_block([(i, m) for i in range(K) for m in range(NH)], "xi", "hb", False)
+    w("    }")
+    for p in range(K):
+        w(f"    if constexpr (P0 <= {p} && {p} < P1) {{ rU[{p}] = fma(g22, p1[{p}], fma(-g21, p2[{p}], rU[{p}]));"
+          f" rV[{p}] = fma(g11, p2[{p}], fma(-g12, p1[{p}], rV[{p}])); }}")
     w("  }")
     # ---- traces and lifts
     for j in range(3):

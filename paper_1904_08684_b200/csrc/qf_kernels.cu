@@ -398,6 +398,12 @@ struct VGroups {
   static constexpr int value = k == 4 ? QF_VG4 : (k == 3 ? QF_VG3 : 1);
 };
 
+// input-outer volume kernel (k = 4): pressure rows from symmetric products
+// (vol_press; measured k = 4 stage 1007 -> 966 us at N = 512; the row-outer
+// k = 3 path is faster without it: 381 vs 395 us)
+#ifndef QF_VPRESS
+#define QF_VPRESS 1
+#endif
 // orders >= QF_VSPLIT solve the velocity of the new state in its own launch
 #ifndef QF_VSPLIT
 #define QF_VSPLIT 3
@@ -850,8 +856,21 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     }
   }
   const GRow gU{c + K * ld + e, ld, i32}, gV{c + 2 * K * ld + e, ld, i32}, gX{c + e, ld, i32};
-  O::template vol_uv_acc<P0, P1>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12, g * B11,
-                                 r + K, r + 2 * K);
+  if constexpr (QF_VPRESS) {  // advection part, then symmetric-product pressure rows
+    O::template vol_uv_acc<P0, P1, false>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12,
+                                          g * B11, r + K, r + 2 * K);
+    double xi[K], hb[NH];
+#pragma unroll
+    for (int i = 0; i < K; ++i) xi[i] = ldv(c + i * ld + e);
+#pragma unroll
+    for (int i = 0; i < NH; ++i) hb[i] = ldg(T.hb + i * ld + e);
+    const double gs = g * i32;
+    O::template vol_press<P0, P1>(xi, hb, P.hb_linear != 0, gs * B22, gs * B21, gs * B12,
+                                  gs * B11, r + K, r + 2 * K);
+  } else {
+    O::template vol_uv_acc<P0, P1>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12, g * B11,
+                                   r + K, r + 2 * K);
+  }
   if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
     double xi[K], ra[K], rb[K];
 #pragma unroll

@@ -28,8 +28,10 @@ def build(specs):
         print(name, "ok" if r.returncode == 0 else r.stderr[-2000:])
 
 
-def run(orders, n, scen):
-    for so in sorted(VAR.glob("*.so")):
+def run(orders, n, scen, rounds=int(os.environ.get("QF_ROUNDS", "1"))):
+    """Variants interleaved ``rounds`` times (box-to-box and drift noise is
+    ~4 %, so compare within one call)."""
+    for so in [so for _ in range(rounds) for so in sorted(VAR.glob("*.so"))]:
         env = dict(os.environ, QF_LIB=str(so))
         code = (f"import sys; sys.path.insert(0, {str(ROOT)!r}); from tools.order_timing import main; "
                 f"main({n}, orders=({orders},), scen={scen!r})")
