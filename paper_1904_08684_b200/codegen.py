@@ -33,6 +33,10 @@ from .tensors import (LAMBDA_SAMPLES, build_ref_tensors, build_trace_space, edge
 
 GEN_DIR = Path(__file__).resolve().parent / "csrc" / "generated"
 TOL = 1e-15
+# orders whose (input-outer, split) volume kernel takes the pressure rows from
+# vol_press instead of the y_l = T_l w contraction (measured: k = 4 faster,
+# k = 3 row-outer slower)
+PRESS_MINK = 4
 QF_LITERAL_ORDERS = tuple(int(x) for x in __import__("os").environ.get("QF_LITERAL_ORDERS", "3").split(",") if x)
 
 
@@ -95,6 +99,46 @@ def _nz(a) -> bool:
     return abs(a) > TOL
 
 
+def _gen_press(w, rt, K, NH):
+    """vol_press<P0, P1>: pressure rows from symmetric products (see gen_order)."""
+    w("  template <int P0 = 0, int P1 = K, class RT> static __device__ __forceinline__ void"
+      " vol_press(const double* xi, const double* hb, bool hbl, double g22, double g21,"
+      " double g12, double g11, RT rU, RT rV) {")
+    w("    constexpr unsigned R = (1u << P1) - (1u << P0);")
+    w("    double p1[K], p2[K];")
+    w("    #pragma unroll\n    for (int p = 0; p < K; ++p) { p1[p] = 0.0; p2[p] = 0.0; }")
+
+    def _press_block(pairs, xa, xb, half_diag):
+        for (i, m) in pairs:
+            ent = []
+            for p in range(K):
+                f = 0.5 if (half_diag and i == m) else 1.0
+                c1, c2 = f * rt.T[0, p, i, m], f * rt.T[1, p, i, m]
+                if _nz(c1) or _nz(c2):
+                    ent.append((p, c1, c2))
+            if not ent:
+                continue
+            mask = sum(1 << p for p, _, _ in ent)
+            w(f"    if constexpr (({mask}u & R) != 0u) {{ const double q = {xa}[{i}] * {xb}[{m}];")
+            for p, c1, c2 in ent:
+                st = []
+                if _nz(c1):
+                    st.append(f"p1[{p}] = fma({scoef(c1)}, q, p1[{p}]);")
+                if _nz(c2):
+                    st.append(f"p2[{p}] = fma({scoef(c2)}, q, p2[{p}]);")
+                w(f"      if constexpr (P0 <= {p} && {p} < P1) {{ {' '.join(st)} }}")
+            w("    }")
+
+    _press_block([(i, m) for i in range(K) for m in range(i, K)], "xi", "xi", True)
+    w("    if (hbl) {")
+    _press_block([(i, m) for i in range(K) for m in range(NH)], "xi", "hb", False)
+    w("    }")
+    for p in range(K):
+        w(f"    if constexpr (P0 <= {p} && {p} < P1) {{ rU[{p}] = fma(g22, p1[{p}], fma(-g21, p2[{p}], rU[{p}]));"
+          f" rV[{p}] = fma(g11, p2[{p}], fma(-g12, p1[{p}], rV[{p}])); }}")
+    w("  }")
+
+
 def gen_order(k: int) -> str:
     K = K_FUNCS[k]
     NT = k + 1
@@ -155,8 +199,8 @@ def gen_order(k: int) -> str:
         w(f"    r[{p}] = {_sum(terms)};")
     w("  }")
     # ---- U/V rows
-    w("  template <bool PRESS = true, class RT, class CT> static __device__ __forceinline__ void"
-      " vol_uv(CT cU, CT cV, CT xi, const double* a, const double* b, const double* wv,")
+    w("  template <class RT, class CT> static __device__ __forceinline__ void vol_uv(CT cU, CT cV,"
+      " CT xi, const double* a, const double* b, const double* wv,")
     w("      double g22, double g21, double g12, double g11, RT rU, RT rV) {")
     for p in range(K):
         w(f"    {{ double su = 0.0, sv = 0.0;")
@@ -171,8 +215,6 @@ def gen_order(k: int) -> str:
             if zt:
                 w(f"        const double z = {_sum(zt)};")
                 w(f"        su = fma(z, cU[{i}], su); sv = fma(z, cV[{i}], sv);")
-            if y1 or y2:
-                w("        if constexpr (PRESS) {")
             if y1 and y2:
                 w(f"        const double y1 = {_sum(y1)}, y2 = {_sum(y2)};")
                 w(f"        su = fma(xi[{i}], fma(g22, y1, -g21 * y2), su);")
@@ -183,8 +225,6 @@ def gen_order(k: int) -> str:
             elif y2:
                 w(f"        const double y2 = {_sum(y2)};")
                 w(f"        su = fma(-xi[{i}] * g21, y2, su); sv = fma(xi[{i}] * g11, y2, sv);")
-            if y1 or y2:
-                w("        }")
             w("      }")
         w(f"      rU[{p}] = su; rV[{p}] = sv; }}")
     w("  }")
@@ -225,7 +265,7 @@ def gen_order(k: int) -> str:
             if zt:
                 w(f"        const double z = {_sum(zt)};")
                 w(f"        rU[{p}] = fma(z, ci, rU[{p}]); rV[{p}] = fma(z, vi, rV[{p}]);")
-            if y1 or y2:
+            if (y1 or y2) and k >= PRESS_MINK:
                 w("        if constexpr (PRESS) {")
             if y1 and y2:
                 w(f"        const double y1 = {_sum(y1)}, y2 = {_sum(y2)};")
@@ -237,7 +277,7 @@ def gen_order(k: int) -> str:
             elif y2:
                 w(f"        const double y2 = {_sum(y2)};")
                 w(f"        rU[{p}] = fma(-xq * g21, y2, rU[{p}]); rV[{p}] = fma(xq * g11, y2, rV[{p}]);")
-            if y1 or y2:
+            if (y1 or y2) and k >= PRESS_MINK:
                 w("        }")
             w("      }")
         w("    }")
@@ -249,42 +289,10 @@ def gen_order(k: int) -> str:
     #             + sum_{i, m<NH} T_l[p,i,m] xi_i hb_m
     # (about half the multiply-adds of the y_l = T_l w contraction), then
     # U_p += g22 pi_1 - g21 pi_2, V_p += g11 pi_2 - g12 pi_1 (rows [P0, P1))
-    w("  template <int P0 = 0, int P1 = K, class RT> static __device__ __forceinline__ void"
-      " vol_press(const double* xi, const double* hb, bool hbl, double g22, double g21,"
-      " double g12, double g11, RT rU, RT rV) {")
-    w("    constexpr unsigned R = (1u << P1) - (1u << P0);")
-    w("    double p1[K], p2[K];")
-    w("    #pragma unroll\n    for (int p = 0; p < K; ++p) { p1[p] = 0.0; p2[p] = 0.0; }")
-
-    def _press_block(pairs, xa, xb, half_diag):
-        for (i, m) in pairs:
-            ent = []
-            for p in range(K):
-                f = 0.5 if (half_diag and i == m) else 1.0
-                c1, c2 = f * rt.T[0, p, i, m], f * rt.T[1, p, i, m]
-                if _nz(c1) or _nz(c2):
-                    ent.append((p, c1, c2))
-            if not ent:
-                continue
-            mask = sum(1 << p for p, _, _ in ent)
-            w(f"    if constexpr (({mask}u & R) != 0u) {{ const double q = {xa}[{i}] * {xb}[{m}];")
-            for p, c1, c2 in ent:
-                st = []
-                if _nz(c1):
-                    st.append(f"p1[{p}] = fma({scoef(c1)}, q, p1[{p}]);")
-                if _nz(c2):
-                    st.append(f"p2[{p}] = fma({scoef(c2)}, q, p2[{p}]);")
-                w(f"      if constexpr (P0 <= {p} && {p} < P1) {{ {' '.join(st)} }}")
-            w("    }")
-
-    _press_block([(i, m) for i in range(K) for m in range(i, K)], "xi", "xi", True)
-    w("    if (hbl) {")
-    _press_block([(i, m) for i in range(K) for m in range(NH)], "xi", "hb", False)
-    w("    }")
-    for p in range(K):
-        w(f"    if constexpr (P0 <= {p} && {p} < P1) {{ rU[{p}] = fma(g22, p1[{p}], fma(-g21, p2[{p}], rU[{p}]));"
-          f" rV[{p}] = fma(g11, p2[{p}], fma(-g12, p1[{p}], rV[{p}])); }}")
-    w("  }")
+    # (generated for the orders whose volume kernel uses it only, so the
+    # other orders' constant pools and register allocation are unchanged)
+    if k >= PRESS_MINK:
+        _gen_press(w, rt, K, NH)
     # ---- traces and lifts
     for j in range(3):
         # explicit fma chains: the same trace is evaluated by the element's own

@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     }
   }
   const GRow gU{c + K * ld + e, ld, i32}, gV{c + 2 * K * ld + e, ld, i32}, gX{c + e, ld, i32};
-  if constexpr (QF_VPRESS) {  // advection part, then symmetric-product pressure rows
+  if constexpr (QF_VPRESS && k >= 4) {  // advection part, then symmetric-product pressure rows
     O::template vol_uv_acc<P0, P1, false>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12,
                                           g * B11, r + K, r + 2 * K);
     double xi[K], hb[NH];
