@@ -158,6 +158,18 @@ struct Blk {
 #ifndef QF_FAKE_HBT
 #define QF_FAKE_HBT 0
 #endif
+// orders whose stage kernel also exchanges the static h_b edge traces through
+// shared memory (6th trace field: own element from its P1 coefficients in
+// phase A, bit-identical to qf_static; out-of-block neighbours copied from
+// the table in phase A2), so the edge loop issues no global loads
+#ifndef QF_HBS_MAXK
+#define QF_HBS_MAXK 2
+#endif
+template <int k>
+struct FS {
+  static constexpr int value = k <= QF_HBS_MAXK ? 6 : 5;  // trace fields per edge in smem
+};
+
 // Lax-Friedrichs flux moments F[3][NT] of local edge j of element e and the
 // lift scale s = edge length / sqrt(detB) (reference solver.py:561-688).
 template <int k, int BS = Blk<k>::value>
@@ -168,7 +180,8 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
                                           double B11, double B12, double B21, double B22,
                                           double isd, double (&F)[3][Ord<k>::NT], double& s) {
   using O = Ord<k>;
-  constexpr int K = O::K, NT = O::NT, NH = O::NH;
+  constexpr int K = O::K, NT = O::NT, NH = O::NH, NF = FS<k>::value;
+  constexpr bool HS = NF == 6;
   const int64_t ld = T.ld;
   // own outward normal: physical image of the reference edge direction
   const double d1 = j == 0 ? -1.0 : (j == 1 ? 0.0 : 1.0);
@@ -179,12 +192,14 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
 
   double own[6][NT], oth[6][NT];
 #pragma unroll
-  for (int f = 0; f < 5; ++f)
+  for (int f = 0; f < NF; ++f)
 #pragma unroll
-    for (int a = 0; a < NT; ++a) own[f][a] = s_tr[((j * 5 + f) * NT + a) * BS + slot];
+    for (int a = 0; a < NT; ++a) own[f][a] = s_tr[((j * NF + f) * NT + a) * BS + slot];
   // static h_b traces (qf_static): [j*NT + a][ld], mean depth term in row 3*NT
+  if constexpr (!HS) {
 #pragma unroll
-  for (int a = 0; a < NT; ++a) own[5][a] = ldg(T.hbt + (j * NT + a) * ld + e);
+    for (int a = 0; a < NT; ++a) own[5][a] = ldg(T.hbt + (j * NT + a) * ld + e);
+  }
   const double hbm_o = P.hb_linear ? 0.0 : ldg(T.hbt + 3 * NT * ld + e);
   double hbm_n = hbm_o;
 
@@ -192,24 +207,26 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   const double* gp = nullptr;
   if (code >= 0) {
     const int nb = code >> 2, jn = code & 3;
+    if constexpr (!HS) {
 #pragma unroll
-    for (int a = 0; a < NT; ++a) {
-      const double v = QF_FAKE_HBT ? own[5][a] : ldg(T.hbt + (jn * NT + a) * ld + nb);
-      oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
+      for (int a = 0; a < NT; ++a) {
+        const double v = QF_FAKE_HBT ? own[5][a] : ldg(T.hbt + (jn * NT + a) * ld + nb);
+        oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
+      }
     }
     if (!P.hb_linear) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
     if (QF_FAKE_HALO || (nb >= blo && nb < bhi)) {  // neighbour traced by its own thread in phase A
       const int ns = QF_FAKE_HALO ? ((nb - blo) & (BS - 1)) : nb - blo;
 #pragma unroll
-      for (int f = 0; f < 5; ++f)
+      for (int f = 0; f < NF; ++f)
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          const double v = s_tr[((jn * 5 + f) * NT + a) * BS + ns];
+          const double v = s_tr[((jn * NF + f) * NT + a) * BS + ns];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
     } else if (QF_NOFALLBACK || hslot >= 0) {  // out-of-block neighbour, traced in phase A2
 #pragma unroll
-      for (int f = 0; f < 5; ++f)
+      for (int f = 0; f < NF; ++f)
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
           const double v = s_ht[(f * NT + a) * HC + (QF_NOFALLBACK ? max(hslot, 0) : hslot)];
@@ -218,7 +235,14 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     } else {  // request list overflow (rare): gather and trace here, compact code
       const double nisd = rsqrt_fast(det2(ldg(T.geo + nb), ldg(T.geo + ld + nb),
                                      ldg(T.geo + 2 * ld + nb), ldg(T.geo + 3 * ld + nb)));
-      const double* L = s_ht + 5 * NT * HC + jn * K * NT;  // s_L (stage_kernel layout)
+      const double* L = s_ht + NF * NT * HC + jn * K * NT;  // s_L (stage_kernel layout)
+      if constexpr (HS) {
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+          const double v = ldg(T.hbt + (jn * NT + a) * ld + nb);
+          oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
+        }
+      }
 #pragma unroll
       for (int fi = 0; fi < 5; ++fi) {
         const double* src =
@@ -535,7 +559,8 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
 template <int k>
 size_t stage_smem_bytes(int hc) {
   constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
-  return sizeof(double) * (3 * 5 * NT * Blk<k>::value + 5 * NT * hc + 3 * K * NT) +
+  constexpr int NF = FS<k>::value;
+  return sizeof(double) * (3 * NF * NT * Blk<k>::value + NF * NT * hc + 3 * K * NT) +
          sizeof(int) * (hc + 8);
 }
 
@@ -547,9 +572,11 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   constexpr int K = O::K, NH = O::NH, NQ = O::NQ, NT = O::NT, BS = Blk<k>::value;
   const int HC = A.hcap;
   extern __shared__ double smem[];
-  double* s_tr = smem;  // trace exchange [3 edges][5 fields][NT][BS]
-  double* s_ht = s_tr + 3 * 5 * NT * BS;  // out-of-block neighbour traces [5][NT][HC]
-  double* s_L = s_ht + 5 * NT * HC;       // Lambda [3][K][NT] (neighbour edge varies by lane)
+  constexpr int NF = FS<k>::value;  // traced fields per edge: xi U V u v (+ h_b)
+  static_assert(FS<k>::value == 5 || k <= QF_PRE_MAXK, "h_b smem traces need the register preload");
+  double* s_tr = smem;  // trace exchange [3 edges][NF fields][NT][BS]
+  double* s_ht = s_tr + 3 * NF * NT * BS;  // out-of-block neighbour traces [NF][NT][HC]
+  double* s_L = s_ht + NF * NT * HC;       // Lambda [3][K][NT] (neighbour edge varies by lane)
   int* s_req = reinterpret_cast<int*>(s_L + 3 * K * NT);  // [HC] neighbour codes, then count
   const double* s_tab = TB::ptr();  // per-order constants (constant memory, uniform reads)
   const int slot = threadIdx.x;
@@ -611,12 +638,17 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   // phase A2 work items: (request, field) pairs in request order; item `it`
   // -> request slot / field
   auto item = [&](int it, int& hsl, int& fi) {
-    int le = it / 5, w = 0;
-    fi = it - 5 * le;
+    int le = it / NF, w = 0;
+    fi = it - NF * le;
     while (w < NW - 1 && le >= s_cnt[w]) le -= s_cnt[w++];
     hsl = w * WC + le;
   };
   auto a2_trace = [&](int hsl, int fi, const double* f, const double* g4) {
+    if (NF == 6 && fi == 5) {  // static h_b trace of the neighbour: copied
+#pragma unroll
+      for (int a = 0; a < NT; ++a) s_ht[(5 * NT + a) * HC + hsl] = f[a];
+      return;
+    }
     const int cd = s_req[hsl], jn = cd & 3;
     const double nisd = rsqrt_fast(det2(g4[0], g4[1], g4[2], g4[3]));
     const double* L = s_L + jn * K * NT;
@@ -630,6 +662,12 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   };
   auto a2_load = [&](int hsl, int fi, double* f, double* g4) {
     const int nb = s_req[hsl] >> 2;
+    if (NF == 6 && fi == 5) {
+      const int jn = s_req[hsl] & 3;
+#pragma unroll
+      for (int a = 0; a < NT; ++a) f[a] = ldg(T.hbt + (jn * NT + a) * ld + nb);
+      return;
+    }
     const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
 #pragma unroll
     for (int i = 0; i < K; ++i) f[i] = ldg(src + i * ld + nb);
@@ -645,7 +683,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if (edges) {
     __syncthreads();
 #pragma unroll
-    for (int w = 0; w < NW; ++w) nit += 5 * s_cnt[w];
+    for (int w = 0; w < NW; ++w) nit += NF * s_cnt[w];
     if constexpr (PF) {
       if (slot < nit) {
         item(slot, p_h, p_f);
@@ -658,7 +696,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     // phase A: own trace moments on all three local edges -> shared memory
     double t3[NT], fl[PRE ? 1 : K];
 #pragma unroll
-    for (int fi = 0; fi < 5; ++fi) {
+    for (int fi = 0; fi < NF; ++fi) {  // (fi = 5: P1 h_b, as qf_static computes it)
       const double* f;
       if constexpr (PRE) {
         f = own_f + fi * K;
@@ -670,13 +708,13 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       }
       O::trace0(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((0 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((0 * NF + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
       O::trace1(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((1 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((1 * NF + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
       O::trace2(f, t3);
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_tr[((2 * 5 + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
+      for (int a = 0; a < NT; ++a) s_tr[((2 * NF + fi) * NT + a) * BS + slot] = __dmul_rn(t3[a], isd);
     }
   }
   if (edges) {
