@@ -77,6 +77,15 @@ typedef struct qf_desc {
 
 typedef struct qf_ctx qf_ctx;
 
+/* Destination buffers of one peer partition for the fused halo push: its
+ * stage-output state c[3][K][ld] and u[2][K][ld] (device pointers: same GPU,
+ * peer-accessible, or mapped with qf_ipc_import). */
+typedef struct qf_peer {
+  double* c;
+  double* u;
+  int64_t ld;
+} qf_peer;
+
 /* Discretization.__init__ (solver.py:103-124): bind tables, validate. */
 int qf_create(const qf_desc* desc, qf_ctx** out);
 void qf_destroy(qf_ctx* ctx);
@@ -112,6 +121,31 @@ int qf_rhs(qf_ctx* ctx, const double* c, const double* u, double t, int32_t term
 int qf_stage(qf_ctx* ctx, const double* c_in, const double* u_in, const double* c0,
              double* c_out, double* u_out, double a, double b, double t, double dt,
              const double* t_dev, double toff, int32_t e0, int32_t n, void* stream);
+
+/* qf_stage with the halo exchange fused into the stage (replaces
+ * the reference-less gather -> send/recv -> scatter of a partitioned run):
+ * the thread that computes a cut-adjacent element's new (c, u) also stores
+ * them into the halo slots of the peers that hold it.  push (device int32
+ * [3][ld], may be NULL): per element up to three destinations
+ * (peer << 26) | peer slot, or -1; peers: device qf_peer table indexed by
+ * peer.  Ordering with the peers' next stage is the caller's (stream order
+ * on one GPU, qf_signal / qf_wait across processes). */
+int qf_stage_push(qf_ctx* ctx, const double* c_in, const double* u_in, const double* c0,
+                  double* c_out, double* u_out, double a, double b, double t, double dt,
+                  const double* t_dev, double toff, int32_t e0, int32_t n, const int32_t* push,
+                  const qf_peer* peers, void* stream);
+
+/* Stream-ordered 32-bit flag write (local or peer memory) and wait until
+ * (int32)(*flag - value) >= 0: cross-process stage ordering of the fused
+ * halo push (stream memory operations, no spinning kernel). */
+int qf_signal(uint32_t* flag, uint32_t value, void* stream);
+int qf_wait(const uint32_t* flag, uint32_t value, void* stream);
+
+/* CUDA IPC of device buffers: handle (64 bytes) + offset of ptr inside its
+ * allocation; import maps a peer's allocation once per process. */
+int qf_ipc_export(const void* ptr, void* handle, uint64_t* offset);
+int qf_ipc_import(const void* handle, uint64_t offset, void** ptr);
+int qf_ipc_close_all(void);
 
 /* Discretization.step (solver.py:745-770): one SSP-RK step in place on
  * (c, u); `u` must hold velocity(c) on entry (qf_velocity).  `work` holds

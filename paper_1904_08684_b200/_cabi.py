@@ -22,6 +22,7 @@ TERM_VOLUME, TERM_EDGE, TERM_SOURCE, TERM_ALL = 1, 2, 4, 7
 EXPORTS = (
     "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
     "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error",
+    "qf_stage_push", "qf_signal", "qf_wait", "qf_ipc_export", "qf_ipc_import", "qf_ipc_close_all",
     "qf_launch_count", "qf_last_error", "qf_abi_version",
 )
 
@@ -69,11 +70,20 @@ def load(path: Path | None = None):
         "qf_error": (C.c_int, [vp, C.POINTER(C.c_uint32), i32, vp]),
         "qf_fill": (C.c_int, [vp, C.c_size_t, d, vp]),
         "qf_l2_error": (C.c_int, [vp, vp, d, i32, i32, vp, vp]),
+        "qf_stage_push": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp, vp,
+                                    vp]),
+        "qf_signal": (C.c_int, [vp, C.c_uint32, vp]),
+        "qf_wait": (C.c_int, [vp, C.c_uint32, vp]),
+        "qf_ipc_export": (C.c_int, [vp, vp, C.POINTER(C.c_uint64)]),
+        "qf_ipc_import": (C.c_int, [vp, C.c_uint64, C.POINTER(C.c_void_p)]),
+        "qf_ipc_close_all": (C.c_int, []),
         "qf_launch_count": (C.c_uint64, []),
         "qf_last_error": (C.c_char_p, []),
         "qf_abi_version": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("QF_LIB") and not hasattr(lib, name):
+            continue  # diagnostic builds of older sources (tools/variants.py)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -33,7 +33,7 @@ import numpy as np
 from .mesh import Mesh
 
 __all__ = ["strip_partition", "block_partition", "range_partition", "Halo", "build_halo",
-           "HaloExchange", "DistributedRunner", "bench_distributed"]
+           "HaloExchange", "push_table", "DistributedRunner", "bench_distributed"]
 
 
 # --------------------------------------------------------------- partitions
@@ -99,6 +99,40 @@ def build_halo(mesh: Mesh, part: np.ndarray, rank: int) -> Halo:
         mine = np.sort(mine)
         send[int(p)] = np.array([g2l[int(g)] for g in mine], dtype=np.int64)
     return Halo(rank=rank, elements=elements, n_own=n_own, n_int=n_int, send=send, recv=recv)
+
+
+PUSH_SLOT_BITS = 26
+
+
+def push_table(halo: Halo, peer_recv: dict, ld: int) -> np.ndarray:
+    """Destinations of the fused halo push (``qf_stage_push``): int32 [3][ld],
+    entry (peer << 26) | slot in the peer's local order, -1 = none.
+
+    ``peer_recv[p]`` is peer p's ``halo.recv[my rank]``: its halo slots of my
+    elements, in the same (global-id) order as my ``halo.send[p]``.  An
+    element adjacent to several peers gets one entry per peer (at most 3:
+    one per edge)."""
+    tab = np.full((3, ld), -1, dtype=np.int32)
+    fill = np.zeros(ld, dtype=np.int64)
+    for p, mine in halo.send.items():
+        dst = np.asarray(peer_recv[p], dtype=np.int64)
+        if len(dst) != len(mine):
+            raise ValueError(f"halo lists of rank {halo.rank} and peer {p} disagree")
+        if p >= 1 << (31 - PUSH_SLOT_BITS) or (len(dst) and dst.max() >= 1 << PUSH_SLOT_BITS):
+            raise ValueError("push table overflow (peer or slot index)")
+        for e, d in zip(np.asarray(mine, dtype=np.int64), dst):
+            tab[fill[e], e] = (p << PUSH_SLOT_BITS) | int(d)
+            fill[e] += 1
+    return tab
+
+
+def peer_table(torch, entries, device):
+    """Device qf_peer[] table: entries[p] = (c_ptr, u_ptr, ld) or None."""
+    t = torch.zeros((max(len(entries), 1), 3), dtype=torch.int64)
+    for p, ent in enumerate(entries):
+        if ent is not None:
+            t[p, 0], t[p, 1], t[p, 2] = int(ent[0]), int(ent[1]), int(ent[2])
+    return t.to(device)
 
 
 # ----------------------------------------------------------------- exchange
@@ -226,10 +260,11 @@ class PartitionRunner:
         if d.tables.bnd_elem.size:
             self.lib.qf_ghost(d._ctx, self.t + rk_plan(self.k)[si][4] * self.dt, stream.cuda_stream)
 
-    def stage(self, si: int, part: str, stream, ghost: bool = True):
+    def stage(self, si: int, part: str, stream, ghost: bool = True, push=None, peers=None):
         """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range
         (with ``ghost``, the interior / all launch is preceded by the stage's
-        Dirichlet data)."""
+        Dirichlet data).  ``push``/``peers`` (device tensors): fused halo push
+        of the new cut-adjacent rows into the peers' stage-output buffers."""
         src, dst, a, b, toff = rk_plan(self.k)[si]
         d, lib, h = self.disc, self.lib, self.halo
         s = stream.cuda_stream
@@ -240,7 +275,12 @@ class PartitionRunner:
         co, uo = self.bufs[dst]
         e0, n = {"interior": (0, h.n_int), "boundary": (h.n_int, h.n_own - h.n_int),
                  "all": (0, h.n_own)}[part]
-        if n > 0:
+        if n > 0 and push is not None:
+            d._check(lib.qf_stage_push(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
+                                       co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None,
+                                       0.0, e0, n, push.data_ptr(), peers.data_ptr(), s),
+                     "qf_stage_push")
+        elif n > 0:
             d._check(lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
                                   co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None, 0.0, e0,
                                   n, s), "qf_stage")
@@ -259,13 +299,23 @@ class DistributedRunner(PartitionRunner):
     """One rank of a partitioned run (one process per GPU, NCCL P2P halos)."""
 
     def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int,
-                 world: int):
+                 world: int, transport: str = "nccl"):
         import torch
         import torch.distributed as dist
 
         super().__init__(mesh, scenario, order, part, rank)
         self.dist, self.rank, self.world = dist, rank, world
-        self.ex = HaloExchange(self.halo, self.K, self.ld, self.disc.device, lib=self.lib)
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
+        if transport == "p2p" and order == 0:
+            # (Euler copies the stage output back over the halo rows a peer may
+            # still be pushing into)
+            raise NotImplementedError("p2p transport needs k >= 1")
+        self.transport = transport
+        if transport == "nccl":
+            self.ex = HaloExchange(self.halo, self.K, self.ld, self.disc.device, lib=self.lib)
+        else:
+            self._setup_p2p(mesh, part)
         if scenario.cfl is not None:
             lmax = torch.tensor([self.local_lambda_max()], dtype=torch.float64, device="cuda")
             hmin = torch.tensor([self.disc.h_min], dtype=torch.float64, device="cuda")
@@ -275,6 +325,68 @@ class DistributedRunner(PartitionRunner):
             self.dt = cfl_time_step(scenario.cfl, order, float(hmin.item()), float(lmax.item()))
         self.comm = torch.cuda.Stream()
         self.bnd = torch.cuda.Stream()
+
+    def _setup_p2p(self, mesh, part):
+        """Fused transport: map the peers' stage buffers (CUDA IPC over
+        NVLink) and build the push table; per stage the cut-adjacent launch
+        stores its new rows straight into the peers' halo slots and raises a
+        per-peer flag (stream memory operation); the peer's next cut-adjacent
+        launch waits on that flag (no NCCL, no gather / scatter kernels)."""
+        import ctypes as C
+
+        torch, dist, lib = self.torch, self.dist, self.lib
+        h = self.halo
+        self.peers = sorted(set(h.send) | set(h.recv))
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device=self.disc.device)
+        bufs = [t for b in range(3) for t in self.bufs[b]] + [self.flags]
+        mine = []
+        for t in bufs:
+            hd = (C.c_char * 64)()
+            off = C.c_uint64(0)
+            _check = self.disc._check
+            _check(lib.qf_ipc_export(t.data_ptr(), hd, C.byref(off)), "qf_ipc_export")
+            mine.append((bytes(hd), int(off.value)))
+        info = [None] * self.world
+        dist.all_gather_object(info, {"ipc": mine, "recv": {int(p): v.tolist()
+                                                            for p, v in h.recv.items()},
+                                      "ld": self.ld})
+        ptrs = {}
+        for p in self.peers:
+            got = []
+            for hd, off in info[p]["ipc"]:
+                ptr = C.c_void_p()
+                self.disc._check(lib.qf_ipc_import(hd, off, C.byref(ptr)), "qf_ipc_import")
+                got.append(ptr.value)
+            ptrs[p] = got
+        dev = self.disc.device
+        self.push = torch.as_tensor(push_table(h, {p: info[p]["recv"][self.rank] for p in h.send},
+                                               self.ld), device=dev)
+        self.peer_bufs = [peer_table(torch, [(ptrs[p][2 * b], ptrs[p][2 * b + 1], info[p]["ld"])
+                                             if p in ptrs else None for p in range(self.world)],
+                                     dev) for b in range(3)]
+        # my flag slot in each peer's flag array
+        self.remote_flag = {p: ptrs[p][6] + 4 * self.rank for p in self.peers}
+        self.gen = 0  # stages completed (flag value)
+
+    def _step_p2p(self):
+        torch, lib = self.torch, self.lib
+        main = torch.cuda.current_stream()
+        for si in range(len(rk_plan(self.k))):
+            self.ghost(si, main)
+            ready = main.record_event()
+            self.stage(si, "interior", main, ghost=False)
+            self.bnd.wait_event(ready)
+            s = self.bnd.cuda_stream
+            for p in self.peers:  # the stage input's halo rows have arrived
+                self.disc._check(lib.qf_wait(self.flags[p:].data_ptr(), self.gen, s), "qf_wait")
+            dst = rk_plan(self.k)[si][1]
+            self.stage(si, "boundary", self.bnd, ghost=False, push=self.push,
+                       peers=self.peer_bufs[dst])
+            self.gen += 1
+            for p in self.peers:
+                self.disc._check(lib.qf_signal(self.remote_flag[p], self.gen, s), "qf_signal")
+            main.wait_stream(self.bnd)
+        self.end_step()
 
     def step(self):
         """One SSP-RK step.  Per stage: the interior range (no halo
@@ -289,6 +401,8 @@ class DistributedRunner(PartitionRunner):
         The two ranges of a stage write disjoint rows and read the stage input
         and the RK base only, the exchange writes halo rows that no interior
         element reads."""
+        if self.transport == "p2p":
+            return self._step_p2p()
         torch = self.torch
         main = torch.cuda.current_stream()
         for si in range(len(rk_plan(self.k))):
@@ -306,7 +420,8 @@ class DistributedRunner(PartitionRunner):
 
     def sync(self):
         main = self.torch.cuda.current_stream()
-        main.wait_stream(self.comm)
+        if self.transport == "nccl":
+            main.wait_stream(self.comm)
         main.wait_stream(self.bnd)
 
 
@@ -315,13 +430,22 @@ class LocalMultiRunner:
     gather/scatter between the partitions' buffers (fake transport for
     single-GPU tests of the partitioned kernels)."""
 
-    def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray):
+    def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray,
+                 transport: str = "gather"):
         import torch
 
         self.torch = torch
         world = int(part.max()) + 1
         self.parts = [PartitionRunner(mesh, scenario, order, part, r) for r in range(world)]
         self.k = order
+        self.transport = transport
+        if transport == "push":  # fused: stage kernels store into each other's halo slots
+            for r, pr in enumerate(self.parts):
+                recv = {p: self.parts[p].halo.recv[r] for p in pr.halo.send}
+                pr.push_tab = torch.as_tensor(push_table(pr.halo, recv, pr.ld), device="cuda")
+                pr.peer_bufs = [peer_table(torch, [(q.bufs[b][0].data_ptr(), q.bufs[b][1].data_ptr(),
+                                                    q.ld) for q in self.parts], "cuda")
+                                for b in range(3)]
         idx = lambda a: torch.as_tensor(a.astype(np.int32), device="cuda")  # noqa: E731
         self.links = []
         for r, pr in enumerate(self.parts):
@@ -332,6 +456,14 @@ class LocalMultiRunner:
     def step(self):
         torch = self.torch
         s = torch.cuda.current_stream()
+        if self.transport == "push":
+            for si in range(len(rk_plan(self.k))):
+                dst = rk_plan(self.k)[si][1]
+                for pr in self.parts:
+                    pr.stage(si, "all", s, push=pr.push_tab, peers=pr.peer_bufs[dst])
+            for pr in self.parts:
+                pr.end_step()
+            return
         for si in range(len(rk_plan(self.k))):
             outs = [pr.stage(si, "all", s) for pr in self.parts]
             for r, p, ridx, sidx in self.links:
@@ -377,7 +509,8 @@ def bench_distributed(args, configs, metric, hooks=None):
     mesh = M.build_unit_square_mesh(n, jitter=jit, seed=7) if jit else M.build_unit_square_mesh(n)
     scn = S.mms_scenario(dt=dt) if scen == "mms" else S.bump_scenario(seed=0, cfl=0.1)
     part = strip_partition(n, world)
-    run = DistributedRunner(mesh, scn, k, part, rank, world)
+    transport = getattr(args, "transport", "nccl")
+    run = DistributedRunner(mesh, scn, k, part, rank, world, transport=transport)
     for _ in range(args.warmup):
         run.step()
     run.sync()
@@ -434,6 +567,7 @@ def bench_distributed(args, configs, metric, hooks=None):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc + f" weak-scaled to N={n}", "order": k, "n": n,
                            "elements": mesh.n_triangles, "parallelism": f"strips x{world}",
+                           "halo_transport": transport,
                            "l2": "flushed (256 MB write) between timed steps"},
                 "gpu_launches": int(launches),
                 "e2e": {"value": 3 * K * mesh.n_triangles * ns * n_e2e / (e2e_t * 1e-3),

@@ -128,6 +128,18 @@ def _torch():
     return torch
 
 
+def _project(vals_w: np.ndarray, phi: np.ndarray) -> np.ndarray:
+    """(E, Q) x (P, Q)^T with a fixed per-row summation order (elementwise
+    accumulation over q), so an element's coefficients do not depend on how
+    many elements are projected together: BLAS GEMM blocking does (k = 4
+    P1 bathymetry differed by 1 ulp between a partition and the whole mesh,
+    which broke bitwise partition independence)."""
+    out = vals_w[:, :1] * phi[:, 0]
+    for q in range(1, vals_w.shape[1]):
+        out = out + vals_w[:, q:q + 1] * phi[:, q]
+    return out
+
+
 class HostSetup:
     """Host-side (NumPy) setup shared by the device path and the CPU tests:
     geometry, quadrature, P1 bathymetry, SoA tables (reference solver.py:103-270)."""
@@ -230,7 +242,7 @@ class HostSetup:
         sd = self.geom.sqrt_detB
         vals = self.scn.hb(self.quad_xy[:, :, 0], self.quad_xy[:, :, 1])
         keep = 1 if self.k == 0 else 3
-        proj = sd[:, None] * ((vals * self.quad_w) @ self.quad_phi[:keep].T)
+        proj = sd[:, None] * _project(vals * self.quad_w, self.quad_phi[:keep])
         self.hb_coef = np.zeros((len(sd), self.K))
         self.hb_coef[:, :keep] = proj
         if keep == 3:
@@ -256,7 +268,7 @@ class HostSetup:
         else:
             raise ValueError("scenario has no analytic solution to project")
         sd = self.geom.sqrt_detB[:, None]
-        c = np.stack([sd * ((f * self.quad_w) @ self.quad_phi.T) for f in fields], axis=1)
+        c = np.stack([sd * _project(f * self.quad_w, self.quad_phi) for f in fields], axis=1)
         H = (self.hb_coef + c[:, XI]) @ self.quad_phi / self.geom.sqrt_detB[:, None]
         if (H < scn.h_min).any():
             raise DryState(f"projected depth fell below h_min = {scn.h_min}")

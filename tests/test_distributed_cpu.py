@@ -124,3 +124,48 @@ def test_halo_lists_are_symmetric():
             for p, ids in h.recv.items():
                 peer = halos[p]
                 assert np.array_equal(h.elements[ids], peer.elements[peer.send[h.rank]])
+
+
+@pytest.mark.parametrize("part", ["strips", "blocks", "ranges"])
+def test_push_tables_fill_every_halo_slot_once(part):
+    """Fused halo push (qf_stage_push) tables: emulating the kernel's stores
+    (every owned element -> its (peer, slot) entries) fills each rank's halo
+    slots exactly once, with the global element the slot stands for."""
+    n = 12
+    mesh = M.build_unit_square_mesh(n)
+    p = {"strips": D.strip_partition(n, 3), "blocks": D.block_partition(n, 2, 2),
+         "ranges": D.range_partition(mesh.n_triangles, 3)}[part]
+    world = int(p.max()) + 1
+    halos = [D.build_halo(mesh, p, r) for r in range(world)]
+    got = [np.full(h.n_local, -1, dtype=np.int64) for h in halos]
+    hits = [np.zeros(h.n_local, dtype=np.int64) for h in halos]
+    for r, h in enumerate(halos):
+        ld = (h.n_local + 31) // 32 * 32
+        tab = D.push_table(h, {q: halos[q].recv[r] for q in h.send}, ld)
+        assert tab.shape == (3, ld) and (tab[:, h.n_own:] == -1).all()
+        assert (tab[:, : h.n_int] == -1).all()  # interior elements push nothing
+        for j in range(3):
+            for e in np.flatnonzero(tab[j] >= 0):
+                q, slot = tab[j, e] >> D.PUSH_SLOT_BITS, tab[j, e] & ((1 << D.PUSH_SLOT_BITS) - 1)
+                got[q][slot] = h.elements[e]
+                hits[q][slot] += 1
+    for h, g, c in zip(halos, got, hits):
+        assert (c[h.n_own:] == 1).all() and (c[: h.n_own] == 0).all()
+        assert np.array_equal(g[h.n_own:], h.elements[h.n_own:])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_host_setup_partition_independent(k):
+    """Host projections (P1 bathymetry, initial state) of a partition equal
+    the whole-mesh ones bit for bit (fixed per-row summation order)."""
+    n = 16
+    mesh = M.build_unit_square_mesh(n)
+    for scn in (S.bump_scenario(seed=0, dt=2e-4, cfl=None), S.mms_scenario(dt=1e-4)):
+        full = HostSetup(mesh, scn, k)
+        fc = full.project_fields()
+        for p in (D.block_partition(n, 2, 2), D.range_partition(mesh.n_triangles, 5)):
+            for r in range(int(p.max()) + 1):
+                h = D.build_halo(mesh, p, r)
+                hs = HostSetup(mesh, scn, k, elements=h.elements, n_own=h.n_own)
+                assert np.array_equal(hs.hb_coef, full.hb_coef[h.elements])
+                assert np.array_equal(hs.project_fields(), fc[h.elements])

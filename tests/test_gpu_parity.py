@@ -128,11 +128,14 @@ def test_p4_mms_vs_oracle():
     assert field_rel(out.c, ref) < TOL
 
 
+@pytest.mark.parametrize("transport", ["gather", "push"])
 @pytest.mark.parametrize("k,case,part", [(2, "mms", "strips"), (3, "walls", "blocks"),
-                                         (1, "mms", "ranges")])
-def test_partitioned_gpu_equals_single_domain(k, case, part):
-    """Partitioned stage kernels + device halo gather/scatter (in-process
-    transport) reproduce the single-domain GPU run bit for bit."""
+                                         (1, "mms", "ranges"), (4, "walls", "blocks")])
+def test_partitioned_gpu_equals_single_domain(k, case, part, transport):
+    """Partitioned stage kernels reproduce the single-domain GPU run bit for
+    bit, with the halo moved by device gather/scatter or by the fused push
+    (qf_stage_push: the stage / velocity kernel stores the new cut-adjacent
+    rows straight into the other partitions' halo slots)."""
     from paper_1904_08684_b200 import distributed as D, mesh as M, scenario as S
     n, steps = 16, 4
     mesh = M.build_unit_square_mesh(n)
@@ -141,7 +144,7 @@ def test_partitioned_gpu_equals_single_domain(k, case, part):
     out = disc.run(disc.project_initial(), t_end=steps * scn.dt)
     p = {"strips": D.strip_partition(n, 4), "blocks": D.block_partition(n, 2, 2),
          "ranges": D.range_partition(mesh.n_triangles, 3)}[part]
-    run = D.LocalMultiRunner(mesh, scn, k, p)
+    run = D.LocalMultiRunner(mesh, scn, k, p, transport=transport)
     for _ in range(steps):
         run.step()
     got = np.zeros_like(out.c)
