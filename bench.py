@@ -461,9 +461,10 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override mesh resolution")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1 halo exchange: NCCL send/recv, or the fused push (stage kernels "
-                         "store into the peers' halo slots over CUDA IPC / NVLink)")
+    ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
+                    help="N > 1 halo exchange: the fused push (stage kernels store into the "
+                         "peers' halo slots over CUDA IPC / NVLink; all ranks fall back to NCCL "
+                         "together if a peer mapping fails), or NCCL send/recv")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU runner even at world size 1 (smoke test)")
     args = ap.parse_args()

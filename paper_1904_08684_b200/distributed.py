@@ -312,10 +312,13 @@ class DistributedRunner(PartitionRunner):
             # still be pushing into)
             raise NotImplementedError("p2p transport needs k >= 1")
         self.transport = transport
-        if transport == "nccl":
+        self.transport_note = None
+        if transport == "p2p" and not self._setup_p2p(mesh, part):
+            # every rank falls back together (e.g. no peer access between
+            # these GPUs); recorded in the bench line
+            self.transport = "nccl"
+        if self.transport == "nccl":
             self.ex = HaloExchange(self.halo, self.K, self.ld, self.disc.device, lib=self.lib)
-        else:
-            self._setup_p2p(mesh, part)
         if scenario.cfl is not None:
             lmax = torch.tensor([self.local_lambda_max()], dtype=torch.float64, device="cuda")
             hmin = torch.tensor([self.disc.h_min], dtype=torch.float64, device="cuda")
@@ -326,12 +329,14 @@ class DistributedRunner(PartitionRunner):
         self.comm = torch.cuda.Stream()
         self.bnd = torch.cuda.Stream()
 
-    def _setup_p2p(self, mesh, part):
+    def _setup_p2p(self, mesh, part) -> bool:
         """Fused transport: map the peers' stage buffers (CUDA IPC over
         NVLink) and build the push table; per stage the cut-adjacent launch
         stores its new rows straight into the peers' halo slots and raises a
         per-peer flag (stream memory operation); the peer's next cut-adjacent
-        launch waits on that flag (no NCCL, no gather / scatter kernels)."""
+        launch waits on that flag (no NCCL, no gather / scatter kernels).
+        Collective-safe: every rank reaches the same collectives and all
+        ranks agree on the outcome (False: use NCCL)."""
         import ctypes as C
 
         torch, dist, lib = self.torch, self.dist, self.lib
@@ -339,34 +344,60 @@ class DistributedRunner(PartitionRunner):
         self.peers = sorted(set(h.send) | set(h.recv))
         self.flags = torch.zeros(self.world, dtype=torch.int32, device=self.disc.device)
         bufs = [t for b in range(3) for t in self.bufs[b]] + [self.flags]
-        mine = []
-        for t in bufs:
-            hd = (C.c_char * 64)()
-            off = C.c_uint64(0)
-            _check = self.disc._check
-            _check(lib.qf_ipc_export(t.data_ptr(), hd, C.byref(off)), "qf_ipc_export")
-            mine.append((bytes(hd), int(off.value)))
+        mine, err = [], None
+        try:
+            for t in bufs:
+                hd = (C.c_char * 64)()
+                off = C.c_uint64(0)
+                self.disc._check(lib.qf_ipc_export(t.data_ptr(), hd, C.byref(off)),
+                                 "qf_ipc_export")
+                mine.append((bytes(hd), int(off.value)))
+        except Exception as exc:  # noqa: BLE001 (reported, all ranks fall back)
+            err, mine = exc, None
         info = [None] * self.world
         dist.all_gather_object(info, {"ipc": mine, "recv": {int(p): v.tolist()
                                                             for p, v in h.recv.items()},
                                       "ld": self.ld})
-        ptrs = {}
-        for p in self.peers:
-            got = []
-            for hd, off in info[p]["ipc"]:
-                ptr = C.c_void_p()
-                self.disc._check(lib.qf_ipc_import(hd, off, C.byref(ptr)), "qf_ipc_import")
-                got.append(ptr.value)
-            ptrs[p] = got
-        dev = self.disc.device
-        self.push = torch.as_tensor(push_table(h, {p: info[p]["recv"][self.rank] for p in h.send},
-                                               self.ld), device=dev)
-        self.peer_bufs = [peer_table(torch, [(ptrs[p][2 * b], ptrs[p][2 * b + 1], info[p]["ld"])
-                                             if p in ptrs else None for p in range(self.world)],
-                                     dev) for b in range(3)]
-        # my flag slot in each peer's flag array
-        self.remote_flag = {p: ptrs[p][6] + 4 * self.rank for p in self.peers}
+        try:
+            if err is not None:
+                raise err
+            if any(info[p]["ipc"] is None for p in self.peers):
+                raise RuntimeError("a peer could not export its buffers")
+            ptrs = {}
+            for p in self.peers:
+                got = []
+                for hd, off in info[p]["ipc"]:
+                    ptr = C.c_void_p()
+                    self.disc._check(lib.qf_ipc_import(hd, off, C.byref(ptr)), "qf_ipc_import")
+                    got.append(ptr.value)
+                ptrs[p] = got
+            dev = self.disc.device
+            self.push = torch.as_tensor(push_table(h, {p: info[p]["recv"][self.rank]
+                                                       for p in h.send}, self.ld), device=dev)
+            self.peer_bufs = [peer_table(torch, [(ptrs[p][2 * b], ptrs[p][2 * b + 1],
+                                                  info[p]["ld"]) if p in ptrs else None
+                                                 for p in range(self.world)], dev)
+                              for b in range(3)]
+            # my flag slot in each peer's flag array; handshake write of 0
+            self.remote_flag = {p: ptrs[p][6] + 4 * self.rank for p in self.peers}
+            s = torch.cuda.current_stream().cuda_stream
+            for p in self.peers:
+                self.disc._check(lib.qf_signal(self.remote_flag[p], 0, s), "qf_signal")
+            torch.cuda.synchronize()
+            ok = 1
+        except Exception as exc:  # noqa: BLE001
+            self.transport_note = f"p2p unavailable on rank {self.rank}: {exc}"
+            ok = 0
+        st = torch.tensor([ok], dtype=torch.int32,
+                          device="cpu" if dist.get_backend() == "gloo" else self.disc.device)
+        dist.all_reduce(st, op=dist.ReduceOp.MIN)
+        dist.barrier()
+        if int(st.item()) == 0:
+            if self.transport_note is None:
+                self.transport_note = "p2p unavailable on another rank"
+            return False
         self.gen = 0  # stages completed (flag value)
+        return True
 
     def _step_p2p(self):
         torch, lib = self.torch, self.lib
@@ -567,7 +598,8 @@ def bench_distributed(args, configs, metric, hooks=None):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc + f" weak-scaled to N={n}", "order": k, "n": n,
                            "elements": mesh.n_triangles, "parallelism": f"strips x{world}",
-                           "halo_transport": transport,
+                           "halo_transport": run.transport,
+                           "halo_transport_note": run.transport_note,
                            "l2": "flushed (256 MB write) between timed steps"},
                 "gpu_launches": int(launches),
                 "e2e": {"value": 3 * K * mesh.n_triangles * ns * n_e2e / (e2e_t * 1e-3),

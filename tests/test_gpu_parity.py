@@ -355,3 +355,20 @@ def test_l2_error_device_rejects_no_exact():
     st = disc.project_initial()
     with pytest.raises(RuntimeError):
         disc.l2_error_sq(st, 0.0)
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_p2p_transport_two_processes(k):
+    """Multi-process fused halo transport (CUDA IPC of the stage buffers,
+    fused push from the stage / velocity kernel, stream-memory-operation
+    flags; no kernel waits on another) with 2 ranks: bit-identical to the
+    single-domain run (tools/p2p_check.py, gloo for the host objects)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                        "--nproc-per-node", "2", os.path.join(root, "tools", "p2p_check.py"),
+                        str(k), "3"], capture_output=True, text=True, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "bit-identical to single domain: True" in r.stdout, r.stdout[-2000:]
