@@ -310,7 +310,7 @@ def run_gpu(args):
         fp64 = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / FP64_PEAK_TFLOPS, "flop_per_elem_stage": prof["flop_per_elem"],
                 "peak_source": "measured DFMA throughput (tools/micro/fp64_pipes.cu)"}
-    e2e = measure_e2e(disc, st0, max(3, min(args.steps, 20)))
+    e2e = measure_e2e(disc, st0, max(3, min(args.steps, 100)))
     cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": world,
@@ -351,9 +351,11 @@ def measure_e2e(disc, st0, steps):
     reference's (E, F, K) State layout).  Every step: H2D of the input state c,
     qf_pack, qf_velocity, qf_step, qf_unpack, D2H of the new state c.
 
-    ``value``: the steps are pipelined over three streams (H2D of step i+1 and
-    D2H of step i-1 overlap the kernels of step i; double-buffered device
-    staging), CUDA events around all K steps.  ``serial``: the same sequence
+    ``value``: the steps are pipelined over three streams (H2D of the next
+    steps and D2H of the previous ones overlap the kernels of step i;
+    double-buffered device staging), CUDA events around all K steps.  Bound:
+    concurrent H2D + D2H of the 8*3*K*E-byte state per step (C2: 0.405 ms per
+    step on the bench box, tools/pcie_bw.py).  ``serial``: the same sequence
     on one stream, each step also reading back u.  Also reports
     Discretization.step (the Python API, numpy in/out) wall clock as
     ``public_api``."""
@@ -368,8 +370,9 @@ def measure_e2e(disc, st0, steps):
     h_out_c = torch.empty((E, 3, K), dtype=torch.float64).pin_memory()
     h_out_u = torch.empty((E, 2, K), dtype=torch.float64).pin_memory()
     h_c.numpy()[:] = st0.c
-    d_in = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(2)]
-    d_out = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(2)]
+    NB = 2  # staging depth (H2D-bound: 2 slots keep the H2D stream busy)
+    d_in = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(NB)]
+    d_out = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(NB)]
     d_u = torch.empty((E, 2, K), dtype=torch.float64, device="cuda")
     c, u = disc._empty_state()
     c.zero_()
@@ -379,10 +382,10 @@ def measure_e2e(disc, st0, steps):
     pp = disc._perm_ptr(E)
     s_cmp = torch.cuda.current_stream()
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]    # H2D into slot done
-    ev_used = [torch.cuda.Event() for _ in range(2)]  # pack consumed slot
-    ev_res = [torch.cuda.Event() for _ in range(2)]   # result unpacked into slot
-    ev_out = [torch.cuda.Event() for _ in range(2)]   # D2H of slot done
+    ev_in = [torch.cuda.Event() for _ in range(NB)]    # H2D into slot done
+    ev_used = [torch.cuda.Event() for _ in range(NB)]  # pack consumed slot
+    ev_res = [torch.cuda.Event() for _ in range(NB)]   # result unpacked into slot
+    ev_out = [torch.cuda.Event() for _ in range(NB)]   # D2H of slot done
 
     def kernels(din, dout, sp, with_u=False):
         _cabi.check(lib.qf_pack(din.data_ptr(), c.data_ptr(), E, 3, K, ld, pp, sp), "pack")
@@ -395,7 +398,7 @@ def measure_e2e(disc, st0, steps):
 
     def pipelined(n):
         for i in range(n):
-            b = i % 2
+            b = i % NB
             with torch.cuda.stream(s_h2d):
                 s_h2d.wait_event(ev_used[b])
                 d_in[b].copy_(h_c, non_blocking=True)
@@ -428,8 +431,9 @@ def measure_e2e(disc, st0, steps):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
-    ms_pipe = timed(pipelined, steps)
-    ms_ser = sum(timed(serial) for _ in range(min(steps, 20))) / min(steps, 20) * steps
+    ms_pipe = timed(pipelined, steps)  # (pipeline fill / drain amortised over the steps)
+    steps = min(steps, 20)
+    ms_ser = sum(timed(serial) for _ in range(steps))
     ns = stages_of(disc.k)
     dof = 3 * K * E * ns
     # the Python API (numpy State in, numpy State out), wall clock
