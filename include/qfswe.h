@@ -115,6 +115,13 @@ int qf_ghost(qf_ctx* ctx, double t, void* stream);
 int qf_rhs(qf_ctx* ctx, const double* c, const double* u, double t, int32_t terms,
            double* rhs, double* lam, void* stream);
 
+/* qf_rhs with Discretization.instrument_mass_flux (solver.py:123-124,
+ * 619-620, 696-701): mflux (device [3][ld]) receives, per element and local
+ * edge, that edge's contribution to the element's xi mode-0 rhs (times
+ * sqrt(detB)/sqrt(2) = the element's mass rate through the edge). */
+int qf_rhs_mass(qf_ctx* ctx, const double* c, const double* u, double t, int32_t terms,
+                double* rhs, double* lam, double* mflux, void* stream);
+
 /* One SSP-RK stage (solver.py:750-764) for elements [e0, e0+n):
  *   c_out = a*c0 + b*(c_in + dt*rhs(c_in, u_in, t)),  u_out = velocity(c_out).
  * t_dev (optional device [2] = {t_step, dt}) overrides t: t = t_dev[0] + toff*t_dev[1]. */

@@ -21,7 +21,7 @@ TERM_VOLUME, TERM_EDGE, TERM_SOURCE, TERM_ALL = 1, 2, 4, 7
 
 EXPORTS = (
     "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
-    "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error",
+    "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error", "qf_rhs_mass",
     "qf_stage_push", "qf_signal", "qf_wait", "qf_ipc_export", "qf_ipc_import", "qf_ipc_close_all",
     "qf_launch_count", "qf_last_error", "qf_abi_version",
 )
@@ -60,6 +60,7 @@ def load(path: Path | None = None):
         "qf_project": (C.c_int, [vp, vp, i32, d, vp, vp, vp]),
         "qf_static": (C.c_int, [vp, i32, vp]),
         "qf_rhs": (C.c_int, [vp, vp, vp, d, i32, vp, vp, vp]),
+        "qf_rhs_mass": (C.c_int, [vp, vp, vp, d, i32, vp, vp, vp, vp]),
         "qf_stage": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp]),
         "qf_step": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "qf_run": (C.c_int, [vp, i32, vp, vp, vp, vp, i32, vp]),

@@ -85,6 +85,7 @@ struct StageArgs {
   const double* vol;              // k >= 3: precomputed volume rhs [3K][ld] (volume_kernel)
   int hcap;                       // out-of-block request slots per block (multiple of BS/32)
   const int* push;                // optional fused halo push [3][ld] (see push_rows)
+  double* mflux;                  // stage_kernel<k, true>: [3][ld] xi mode-0 rhs of each edge
   const qf_peer* peers;           // device table of the peers' destination buffers
 };
 
@@ -410,7 +411,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   s = l2 * il * isd;  // edge length / sqrt(detB)
 }
 
-template <int k, int BS = Blk<k>::value>
+template <int k, int BS = Blk<k>::value, bool MF = false>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
@@ -436,6 +437,18 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     O::lift2(F[0], s, r);
     O::lift2(F[1], s, r + K);
     O::lift2(F[2], s, r + 2 * K);
+  }
+  if constexpr (MF) {  // instrument_mass_flux: this edge's xi mode-0 rhs (solver.py:619-620)
+    double m[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) m[p] = 0.0;
+    if (j == 0)
+      O::lift0(F[0], s, m);
+    else if (j == 1)
+      O::lift1(F[0], s, m);
+    else
+      O::lift2(F[0], s, m);
+    A.mflux[j * T.ld + e] = m[0];
   }
 }
 
@@ -596,7 +609,7 @@ size_t stage_smem_bytes(int hc) {
          sizeof(int) * (hc + 8);
 }
 
-template <int k>
+template <int k, bool MF = false>
 __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
@@ -827,7 +840,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #endif
     QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < QF_FAKE_NEDGE; ++j)  // (timing experiments only: < 3 is wrong numerics)
-      edge_term<k>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
+      edge_term<k, Blk<k>::value, MF>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
   }
   if (A.mode == 0) {
@@ -1383,11 +1396,16 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   if (!attr) {
     cudaFuncSetAttribute(stage_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)stage_smem_bytes<k>(QF_HCAP));
+    cudaFuncSetAttribute(stage_kernel<k, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<k>(QF_HCAP));
     attr = true;
   }
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
-  stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
+  if (a.mflux)  // instrumented instance (mass-flux diagnostics only)
+    stage_kernel<k, true><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
+  else
+    stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
   g_launches++;
   if constexpr (k >= QF_VSPLIT) {
     if (a.mode == 1) {
@@ -1568,6 +1586,11 @@ int qf_ghost(qf_ctx* x, double t, void* stream) {
 
 int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms, double* rhs,
            double* lam, void* stream) {
+  return qf_rhs_mass(x, c, u, t, terms, rhs, lam, nullptr, stream);
+}
+
+int qf_rhs_mass(qf_ctx* x, const double* c, const double* u, double t, int32_t terms,
+                double* rhs, double* lam, double* mflux, void* stream) {
   if (!x || !c || !u || !rhs) return fail(QF_E_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (terms & TERM_EDGE)
@@ -1577,6 +1600,7 @@ int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms,
   a.u = u;
   a.c_out = rhs;
   a.lam = lam;
+  a.mflux = (terms & TERM_EDGE) ? mflux : nullptr;
   a.err = x->err;
   a.t = t;
   a.e0 = 0;

@@ -211,6 +211,10 @@ class HostSetup:
                              "has no device evaluator (use a closed-form scenario family)")
         self._cfl_warned = False
         self.cfl_warn_threshold = 2.0
+        # reference solver.py:123-124: per-interior-edge xi mass flux of the
+        # left / right element, recorded by edge_rhs / rhs when enabled
+        self.instrument_mass_flux: bool = False
+        self.last_mass_flux: tuple | None = None
         self.dt = scenario.dt
         self._dt_fixed = scenario.cfl is None
         self.phi_at_vertices = np.array(
@@ -523,14 +527,34 @@ class Discretization(HostSetup):
         out, _ = self._empty_state()
         lam = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device) \
             if want_lam else None
-        self._check(self._lib.qf_rhs(self._ctx, c.data_ptr(), u.data_ptr(), float(t), terms,
-                                     out.data_ptr(), lam.data_ptr() if want_lam else None,
-                                     self._stream), "qf_rhs")
+        mass = self.instrument_mass_flux and (terms & _cabi.TERM_EDGE) and not self.partitioned
+        mf = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device) \
+            if mass else None
+        self._check(self._lib.qf_rhs_mass(self._ctx, c.data_ptr(), u.data_ptr(), float(t), terms,
+                                          out.data_ptr(), lam.data_ptr() if want_lam else None,
+                                          mf.data_ptr() if mass else None, self._stream),
+                    "qf_rhs_mass")
         self._raise_errors("rhs")
         r = self._soa_to_host(out, 3)
+        if mass:
+            self.last_mass_flux = self._mass_flux_rows(mf[:, : self.tables.n_elem].cpu().numpy())
         if want_lam:
             return r, lam[:, : self.tables.n_elem].cpu().numpy()
         return r
+
+    def _mass_flux_rows(self, mf: np.ndarray):
+        """(mL, mR) over the interior edges in mesh.edges order (reference
+        solver.py:696-701): the element's mass rate sqrt(detB)/sqrt(2) *
+        (xi mode-0 rhs) through the edge, for its left / right element."""
+        if self.perm is not None:
+            rows = np.empty_like(mf)
+            rows[:, self.perm] = mf
+            mf = rows
+        mf = mf * (self.geom.sqrt_detB / math.sqrt(2.0))[None, :]
+        cn = self.mesh.conn
+        inner = np.flatnonzero(cn.right >= 0)
+        return (mf[cn.left_local[inner], cn.left[inner]],
+                mf[cn.right_local[inner], cn.right[inner]])
 
     def compute_lambda(self, state: State, t: float) -> np.ndarray:
         """Per-edge LF speed in ``mesh.edges`` order (solver.py:340-406)."""

@@ -2,7 +2,8 @@
 
 Run in the build container (needs /root/reference, read-only):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py                 # all fixtures
+    python tests/golden/make_golden.py --mass-flux     # massflux_k*.npz only
 
 It imports the reference package under the alias ``qfswe_ref`` (it has no
 ``__init__.py``) and writes small ``.npz`` fixtures next to this
@@ -118,10 +119,26 @@ def tensor_files(R):
     np.savez_compressed(HERE / "tensor_files.npz", **out)
 
 
+def mass_flux(R):
+    """instrument_mass_flux / last_mass_flux of edge_rhs (solver.py:123-124,
+    619-620, 696-701) on the perturbed states of square_k{k}.npz, k = 1..3."""
+    mesh = R.mesh.build_square_mesh(3, 0.2, 42)
+    for k in (1, 2, 3):
+        g = np.load(HERE / f"square_k{k}.npz")
+        disc = R.solver.Discretization(mesh, R.scenario.perturbed_square_scenario(dt=0.5), k)
+        disc.instrument_mass_flux = True
+        st = R.solver.State(c=g["cr"].copy(), u=g["ur"].copy(), t=0.0)
+        disc.edge_rhs(st, 3.7)
+        mL, mR = disc.last_mass_flux
+        np.savez_compressed(HERE / f"massflux_k{k}.npz", mL=mL, mR=mR)
+
+
 def main():
     R = load_reference()
     if "--tensor-files" in sys.argv:
         return tensor_files(R)
+    if "--mass-flux" in sys.argv:
+        return mass_flux(R)
     # A. tensors
     for k in range(4):
         t = R.tensors.build_ref_tensors(k)

@@ -372,3 +372,23 @@ def test_p2p_transport_two_processes(k):
                         str(k), "3"], capture_output=True, text=True, timeout=240, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "bit-identical to single domain: True" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_mass_flux_instrumentation_vs_reference(golden, k):
+    """instrument_mass_flux / last_mass_flux (reference solver.py:123-124,
+    619-620, 696-701): per-interior-edge xi mass flux of the left and right
+    element equals the reference's (tests/golden/massflux_k{k}.npz), and the
+    two sides cancel (conservation)."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import State
+    g, gs = golden(f"massflux_k{k}.npz"), golden(f"square_k{k}.npz")
+    disc = _disc(M.build_square_mesh(3, 0.2, 42), S.perturbed_square_scenario(dt=0.5), k)
+    assert disc.last_mass_flux is None
+    disc.instrument_mass_flux = True
+    disc.edge_rhs(State(gs["cr"].copy(), gs["ur"].copy(), 0.0), 3.7)
+    mL, mR = disc.last_mass_flux
+    scale = np.abs(g["mL"]).max()
+    assert np.abs(mL - g["mL"]).max() <= 1e-11 * scale
+    assert np.abs(mR - g["mR"]).max() <= 1e-11 * scale
+    assert np.abs(mL + mR).max() <= 1e-12 * scale
