@@ -235,6 +235,8 @@ def run_gpu(args):
     st0 = disc.project_initial()
     K, E, ld = disc.K, mesh.n_triangles, disc.ld
     ds = disc.to_device(st0)
+    if st0._dev is not None:  # device-set-up state: step a copy, keep st0 initial
+        ds = ds.clone()
     ds.t_dev[1] = disc.dt
     work = disc._work_buf()
     stream = torch.cuda.current_stream()
@@ -265,6 +267,7 @@ def run_gpu(args):
     launches = lib.qf_launch_count() - n0
     clk = clocks.stop()
     disc._raise_errors("bench")
+    checks = state_checks(disc, st0, ds, E)
     # ---- pass B (roofline): the same stages with an event pair around each
     # stage_kernel launch (qf_stage), L2 flushed between steps as in pass A
     S5, S3 = 5 * K * ld, 3 * K * ld
@@ -310,7 +313,7 @@ def run_gpu(args):
         fp64 = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / FP64_PEAK_TFLOPS, "flop_per_elem_stage": prof["flop_per_elem"],
                 "peak_source": "measured DFMA throughput (tools/micro/fp64_pipes.cu)"}
-    e2e = measure_e2e(disc, st0, max(3, min(args.steps, 100)))
+    e2e = None if args.no_e2e else measure_e2e(disc, st0, max(3, min(args.steps, 100)))
     cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": world,
@@ -338,12 +341,30 @@ def run_gpu(args):
         "hbm_roofline_dof_per_s": 3 * K * E * ns / (bytes_step / (peak * 1e9)),
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "checks": checks,
         "clocks": clk,
     }
     line["roofline_frac_dof"] = value / line["hbm_roofline_dof_per_s"]
     if cb is not None:
         line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
+
+
+def state_checks(disc, st0, ds, E):
+    """Size-independent properties of the full-size run after the timed
+    steps: xi mass conservation on wall configurations, the L2
+    error against the exact solution (qf_l2_error) on manufactured ones."""
+    t_end = float(ds.t_dev[0].item())
+    out = {"t": t_end, "steps_run": int(round(t_end / disc.dt))}
+    geo = disc.tables.geo
+    sd = np.sqrt(geo[0, :E] * geo[3, :E] - geo[1, :E] * geo[2, :E])
+    m_end = ds.c[0, 0, :E].cpu().numpy() * sd / np.sqrt(2.0)
+    m0 = st0.c[:, 0, 0] * disc.geom.sqrt_detB / np.sqrt(2.0)
+    if disc.tables.bnd_elem.size == 0:
+        out["xi_mass_drift_rel"] = float(abs(m_end.sum() - m0.sum()) / np.abs(m0).sum())
+    if getattr(disc.scn.device, "kind", 0) != 0 and disc.scn.exact is not None:
+        out["l2_error_xi_U_V"] = [float(v) for v in np.sqrt(disc.l2_error_sq(ds, t_end))]
+    return out
 
 
 def measure_e2e(disc, st0, steps):
@@ -465,6 +486,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override mesh resolution")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the host-buffer legs (diagnostic runs at sizes whose host "
+                         "State is tens of GB, e.g. C5 strong on one GPU)")
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
                     help="N > 1 halo exchange: the fused push (stage kernels store into the "
                          "peers' halo slots over CUDA IPC / NVLink; all ranks fall back to NCCL "
