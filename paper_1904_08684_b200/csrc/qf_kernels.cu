@@ -467,6 +467,12 @@ struct VGroups {
   static constexpr int value = k == 4 ? QF_VG4 : (k == 3 ? QF_VG3 : 1);
 };
 
+// orders (bit mask) whose scenarios without manufactured forcing launch a
+// stage-kernel instance without the forcing code (measured at N = 512:
+// k = 3 381 -> 370 us; k = 1, 2 slower, k = 4 equal)
+#ifndef QF_NOFORCE_INST
+#define QF_NOFORCE_INST 8
+#endif
 // input-outer volume kernel (k = 4): pressure rows from symmetric products
 // (vol_press; measured k = 4 stage 1007 -> 966 us at N = 512; the row-outer
 // k = 3 path is faster without it: 381 vs 395 us)
@@ -609,7 +615,10 @@ size_t stage_smem_bytes(int hc) {
          sizeof(int) * (hc + 8);
 }
 
-template <int k, bool MF = false>
+// MF: mass-flux instrumentation; FC: the manufactured-forcing code is
+// compiled in (instances without it are launched for scenarios without
+// forcing: a smaller register / spill footprint)
+template <int k, bool MF = false, bool FC = true>
 __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
@@ -821,7 +830,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
       r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
     }
-    if (P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
+    if (FC && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
       forcing_quad<k>(P, T, e, t, B11, B12, B21, B22, sd,
                       [&](const double* Pq, double S, double Fx, double Fy) {
 #pragma unroll
@@ -1398,14 +1407,19 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
                          (int)stage_smem_bytes<k>(QF_HCAP));
     cudaFuncSetAttribute(stage_kernel<k, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)stage_smem_bytes<k>(QF_HCAP));
+    cudaFuncSetAttribute(stage_kernel<k, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<k>(QF_HCAP));
     attr = true;
   }
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
   if (a.mflux)  // instrumented instance (mass-flux diagnostics only)
     stage_kernel<k, true><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
-  else
+  else if (x->phys.forcing || !((QF_NOFORCE_INST >> k) & 1))
     stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
+  else
+    stage_kernel<k, false, false><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
   g_launches++;
   if constexpr (k >= QF_VSPLIT) {
     if (a.mode == 1) {
