@@ -205,7 +205,7 @@ struct FS {
 
 // Lax-Friedrichs flux moments F[3][NT] of local edge j of element e and the
 // lift scale s = edge length / sqrt(detB) (reference solver.py:561-688).
-template <int k, int BS = Blk<k>::value>
+template <int k, int BS = Blk<k>::value, bool DIR = true, bool HBC = true>
 __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
@@ -233,7 +233,9 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
 #pragma unroll
     for (int a = 0; a < NT; ++a) own[5][a] = ldg(T.hbt + (j * NT + a) * ld + e);
   }
-  const double hbm_o = P.hb_linear ? 0.0 : ldg(T.hbt + 3 * NT * ld + e);
+  // DIR / HBC = false: instances without the Dirichlet-ghost / constant-h_b code
+  const bool hbl = !HBC || P.hb_linear;
+  const double hbm_o = hbl ? 0.0 : ldg(T.hbt + 3 * NT * ld + e);
   double hbm_n = hbm_o;
 
   bool dirichlet = false;
@@ -247,7 +249,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
         oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
       }
     }
-    if (!P.hb_linear) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
+    if (!hbl) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
     if (QF_FAKE_HALO || (nb >= blo && nb < bhi)) {  // neighbour traced by its own thread in phase A
       const int ns = QF_FAKE_HALO ? ((nb - blo) & (BS - 1)) : nb - blo;
 #pragma unroll
@@ -306,7 +308,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     }
   } else {
     const int v = -1 - code, bslot = v >> 1;
-    if ((v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
+    if (DIR && (v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
       using TB = Tabs<k>;
       constexpr int NG = O::NG;
       dirichlet = true;
@@ -389,8 +391,8 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   double wO[NT], wN[NT], pO[NT], pN[NT], aO[NT], aN[NT], bO[NT], bN[NT];
 #pragma unroll
   for (int a = 0; a < NT; ++a) {
-    wO[a] = 0.5 * own[0][a] + (P.hb_linear ? own[5][a] : 0.0);
-    wN[a] = 0.5 * oth[0][a] + (P.hb_linear ? oth[5][a] : 0.0);
+    wO[a] = 0.5 * own[0][a] + (hbl ? own[5][a] : 0.0);
+    wN[a] = 0.5 * oth[0][a] + (hbl ? oth[5][a] : 0.0);
   }
   O::jprod(own[0], wO, pO);
   O::jprod(oth[0], wN, pN);
@@ -402,7 +404,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
 #pragma unroll
   for (int a = 0; a < NT; ++a) {
     double pr = pO[a] + pN[a];
-    if (!P.hb_linear) pr += hbm_o * own[0][a] + hbm_n * oth[0][a];
+    if (!hbl) pr += hbm_o * own[0][a] + hbm_n * oth[0][a];
     F[0][a] = 0.5 * (n1 * (own[1][a] + oth[1][a]) + n2 * (own[2][a] + oth[2][a])) +
               hl * (own[0][a] - oth[0][a]);
     F[1][a] = 0.5 * (aO[a] + aN[a] + g * n1 * pr) + hl * (own[1][a] - oth[1][a]);
@@ -411,7 +413,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   s = l2 * il * isd;  // edge length / sqrt(detB)
 }
 
-template <int k, int BS = Blk<k>::value, bool MF = false>
+template <int k, int BS = Blk<k>::value, bool MF = false, bool DIR = true, bool HBC = true>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
@@ -422,7 +424,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   using O = Ord<k>;
   constexpr int K = O::K, NT = O::NT;
   double F[3][NT], s;
-  edge_flux<k, BS>(T, P, A, e, j, code, slot, blo, bhi, s_tr, s_ht, hslot, HC, B11, B12, B21, B22,
+  edge_flux<k, BS, DIR, HBC>(T, P, A, e, j, code, slot, blo, bhi, s_tr, s_ht, hslot, HC, B11, B12, B21, B22,
                    isd, F, s);
   // lift: r_f[p] -= (len / sqrt(detB)) sum_a Lambda_j[p, a] F_f[a]
   if (j == 0) {
@@ -473,6 +475,13 @@ struct VGroups {
 #ifndef QF_NOFORCE_INST
 #define QF_NOFORCE_INST 8
 #endif
+// orders (bit mask) that launch lean instances for hb_mode "linear": without
+// the constant-h_b code, and for wall-only, forcing-free problems also
+// without the Dirichlet-ghost and forcing code (measured at N = 512, walls:
+// k = 1..4 2.5-3.5 % faster)
+#ifndef QF_LEAN_INST
+#define QF_LEAN_INST 30
+#endif
 // input-outer volume kernel (k = 4): pressure rows from symmetric products
 // (vol_press; measured k = 4 stage 1007 -> 966 us at N = 512; the row-outer
 // k = 3 path is faster without it: 381 vs 395 us)
@@ -499,7 +508,7 @@ struct Occ {
 
 // Volume terms, Eqs. (15)-(16) (reference solver.py:410-485, const-h_b form
 // :498-510): factorised stiffness-triple contraction in literal code.
-template <int k>
+template <int k, bool HBC = true>
 __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B12, double B21,
                                              double B22, double isd, double idet,
                                              const double* xi, const double* cU,
@@ -519,7 +528,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
     r[i] += ra[i] * idet;
     al[i] = B22 * u[i] - B12 * u[K + i];   // a
     be[i] = -B21 * u[i] + B11 * u[K + i];  // b
-    wv[i] = 0.5 * xi[i] + (P.hb_linear ? hb[i] : 0.0);
+    wv[i] = 0.5 * xi[i] + ((!HBC || P.hb_linear) ? hb[i] : 0.0);
   }
   const double g = P.g;
   O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
@@ -529,7 +538,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
     r[K + i] += ra[i] * i32;
     r[2 * K + i] += rb[i] * i32;
   }
-  if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+  if (HBC && !P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
     const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -615,10 +624,10 @@ size_t stage_smem_bytes(int hc) {
          sizeof(int) * (hc + 8);
 }
 
-// MF: mass-flux instrumentation; FC: the manufactured-forcing code is
-// compiled in (instances without it are launched for scenarios without
-// forcing: a smaller register / spill footprint)
-template <int k, bool MF = false, bool FC = true>
+// Compile-time instances (smaller register / spill footprint when a code
+// path cannot occur): MF mass-flux instrumentation; FC manufactured
+// forcing; DIR Dirichlet ghosts; HBC hb_mode "const" terms.
+template <int k, bool MF = false, bool FC = true, bool DIR = true, bool HBC = true>
 __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
@@ -814,7 +823,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 
   if constexpr (k <= 2) {
     if (QF_EN_VOL && (A.terms & TERM_VOL))
-      volume_terms<k>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
+      volume_terms<k, HBC>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
   } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
@@ -849,7 +858,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #endif
     QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < QF_FAKE_NEDGE; ++j)  // (timing experiments only: < 3 is wrong numerics)
-      edge_term<k, Blk<k>::value, MF>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
+      edge_term<k, Blk<k>::value, MF, DIR, HBC>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
   }
   if (A.mode == 0) {
@@ -1374,6 +1383,19 @@ static int cuda_check(const char* what) {
     default: FN<4>(__VA_ARGS__); break;    \
   }
 
+// one stage-kernel instance: the dynamic shared-memory opt-in once per instance
+template <int k, bool MF, bool FC, bool DIR, bool HBC>
+static void stage_inst(qf_ctx* x, const StageArgs& a, cudaStream_t s, int grid, size_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stage_kernel<k, MF, FC, DIR, HBC>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<k>(QF_HCAP));
+    attr = true;
+  }
+  stage_kernel<k, MF, FC, DIR, HBC><<<grid, Blk<k>::value, smem, s>>>(x->tab, x->phys, a);
+}
+
 template <int k>
 static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   StageArgs a = a_in;
@@ -1401,25 +1423,20 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   constexpr int bs = Blk<k>::value;
   a.hcap = x->hcap;
   const size_t smem = stage_smem_bytes<k>(a.hcap);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stage_kernel<k>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes<k>(QF_HCAP));
-    cudaFuncSetAttribute(stage_kernel<k, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes<k>(QF_HCAP));
-    cudaFuncSetAttribute(stage_kernel<k, false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes<k>(QF_HCAP));
-    attr = true;
-  }
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
+  const Phys& P = x->phys;
+  const bool lean = P.hb_linear && ((QF_LEAN_INST >> k) & 1);
   if (a.mflux)  // instrumented instance (mass-flux diagnostics only)
-    stage_kernel<k, true><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
-  else if (x->phys.forcing || !((QF_NOFORCE_INST >> k) & 1))
-    stage_kernel<k><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
+    stage_inst<k, true, true, true, true>(x, a, s, grid, smem);
+  else if (lean && P.forcing && x->d.n_bnd > 0)  // manufactured solutions (C1, C2)
+    stage_inst<k, false, true, true, false>(x, a, s, grid, smem);
+  else if (lean && !P.forcing && x->d.n_bnd == 0)  // walls, no forcing (C3-C5)
+    stage_inst<k, false, false, false, false>(x, a, s, grid, smem);
+  else if (!P.forcing && ((QF_NOFORCE_INST >> k) & 1))
+    stage_inst<k, false, false, true, true>(x, a, s, grid, smem);
   else
-    stage_kernel<k, false, false><<<grid, bs, smem, s>>>(x->tab, x->phys, a);
+    stage_inst<k, false, true, true, true>(x, a, s, grid, smem);
   g_launches++;
   if constexpr (k >= QF_VSPLIT) {
     if (a.mode == 1) {
