@@ -191,6 +191,18 @@ struct Blk {
 #ifndef QF_FAKE_HBT
 #define QF_FAKE_HBT 0
 #endif
+// Stage-kernel instance variants (compile-time code paths; a path that cannot
+// occur on a problem is compiled out: smaller register / spill footprint)
+enum : int {
+  V_MF = 1,     // mass-flux instrumentation output
+  V_FC = 2,     // manufactured forcing
+  V_DIR = 4,    // Dirichlet ghosts
+  V_HBC = 8,    // hb_mode "const" terms
+  V_WALL = 16,  // reflective walls
+  V_TAY7 = 32,  // MMS forcing with degree-7 Taylor phases only (no generic forcing code)
+  V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL
+};
+
 // orders whose stage kernel also exchanges the static h_b edge traces through
 // shared memory (6th trace field: own element from its P1 coefficients in
 // phase A, bit-identical to qf_static; out-of-block neighbours copied from
@@ -205,7 +217,7 @@ struct FS {
 
 // Lax-Friedrichs flux moments F[3][NT] of local edge j of element e and the
 // lift scale s = edge length / sqrt(detB) (reference solver.py:561-688).
-template <int k, int BS = Blk<k>::value, bool DIR = true, bool HBC = true>
+template <int k, int BS = Blk<k>::value, int V = V_GENERAL>
 __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
@@ -233,8 +245,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
 #pragma unroll
     for (int a = 0; a < NT; ++a) own[5][a] = ldg(T.hbt + (j * NT + a) * ld + e);
   }
-  // DIR / HBC = false: instances without the Dirichlet-ghost / constant-h_b code
-  const bool hbl = !HBC || P.hb_linear;
+  const bool hbl = !(V & V_HBC) || P.hb_linear;
   const double hbm_o = hbl ? 0.0 : ldg(T.hbt + 3 * NT * ld + e);
   double hbm_n = hbm_o;
 
@@ -308,7 +319,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     }
   } else {
     const int v = -1 - code, bslot = v >> 1;
-    if (DIR && (v & 1) == 0) {  // Dirichlet: ghost traces = Gauss moments of exact data
+    if ((V & V_DIR) && (!(V & V_WALL) || (v & 1) == 0)) {  // Dirichlet: ghost = Gauss moments of exact data
       using TB = Tabs<k>;
       constexpr int NG = O::NG;
       dirichlet = true;
@@ -413,7 +424,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   s = l2 * il * isd;  // edge length / sqrt(detB)
 }
 
-template <int k, int BS = Blk<k>::value, bool MF = false, bool DIR = true, bool HBC = true>
+template <int k, int BS = Blk<k>::value, int V = V_GENERAL>
 __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const StageArgs& A, int e,
                                           int j, int code, int slot, int blo, int bhi,
                                           const double* __restrict__ s_tr,
@@ -424,7 +435,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
   using O = Ord<k>;
   constexpr int K = O::K, NT = O::NT;
   double F[3][NT], s;
-  edge_flux<k, BS, DIR, HBC>(T, P, A, e, j, code, slot, blo, bhi, s_tr, s_ht, hslot, HC, B11, B12, B21, B22,
+  edge_flux<k, BS, V>(T, P, A, e, j, code, slot, blo, bhi, s_tr, s_ht, hslot, HC, B11, B12, B21, B22,
                    isd, F, s);
   // lift: r_f[p] -= (len / sqrt(detB)) sum_a Lambda_j[p, a] F_f[a]
   if (j == 0) {
@@ -440,7 +451,7 @@ __device__ __forceinline__ void edge_term(const Tab& T, const Phys& P, const Sta
     O::lift2(F[1], s, r + K);
     O::lift2(F[2], s, r + 2 * K);
   }
-  if constexpr (MF) {  // instrument_mass_flux: this edge's xi mode-0 rhs (solver.py:619-620)
+  if constexpr ((V & V_MF) != 0) {  // instrument_mass_flux: this edge's xi mode-0 rhs (solver.py:619-620)
     double m[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) m[p] = 0.0;
@@ -508,7 +519,7 @@ struct Occ {
 
 // Volume terms, Eqs. (15)-(16) (reference solver.py:410-485, const-h_b form
 // :498-510): factorised stiffness-triple contraction in literal code.
-template <int k, bool HBC = true>
+template <int k, int V = V_GENERAL>
 __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B12, double B21,
                                              double B22, double isd, double idet,
                                              const double* xi, const double* cU,
@@ -528,7 +539,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
     r[i] += ra[i] * idet;
     al[i] = B22 * u[i] - B12 * u[K + i];   // a
     be[i] = -B21 * u[i] + B11 * u[K + i];  // b
-    wv[i] = 0.5 * xi[i] + ((!HBC || P.hb_linear) ? hb[i] : 0.0);
+    wv[i] = 0.5 * xi[i] + ((!(V & V_HBC) || P.hb_linear) ? hb[i] : 0.0);
   }
   const double g = P.g;
   O::vol_uv(cU, cV, xi, al, be, wv, g * B22, g * B21, g * B12, g * B11, ra, rb);
@@ -538,7 +549,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
     r[K + i] += ra[i] * i32;
     r[2 * K + i] += rb[i] * i32;
   }
-  if (HBC && !P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+  if ((V & V_HBC) && !P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
     const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -563,7 +574,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
 // Manufactured forcing at the (k+2)^2 collapsed Gauss points of element e
 // (reference solver.py:719-724, scenario.py:78-93): sink(P_q, S, Fx, Fy)
 // with P_q[p] = w_q phi_p(q) and the point values already scaled by sqrt(detB).
-template <int k, class Sink>
+template <int k, int V = V_GENERAL, class Sink>
 __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e, double t,
                                              double B11, double B12, double B21, double B22,
                                              double sd, Sink&& sink) {
@@ -577,7 +588,7 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
   // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
   // value by a Taylor-evaluated small angle (2 sincospi per element
   // instead of 2 per quadrature point)
-  const bool tay = P.kind == SCN_MMS && P.taylor;
+  const bool tay = (V & V_TAY7) || (P.kind == SCN_MMS && P.taylor);
   // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
   // the centroid; per point only small-angle Taylor rotations follow
   const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
@@ -595,7 +606,7 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
     if (tay) {
       const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
       double sz, cz, sw, cw;
-      if (P.taylor == 2) {
+      if ((V & V_TAY7) || P.taylor == 2) {
         sincos_small7(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
         sincos_small7(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
       } else {
@@ -606,7 +617,7 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
       forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
                   fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
                   fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
-    } else {
+    } else if constexpr (!(V & V_TAY7)) {
       forcing(P, x, y, t, st, ct, S, Fx, Fy);
     }
     sink(s_tab + TB::P + q * K, S * sd, Fx * sd, Fy * sd);
@@ -624,10 +635,8 @@ size_t stage_smem_bytes(int hc) {
          sizeof(int) * (hc + 8);
 }
 
-// Compile-time instances (smaller register / spill footprint when a code
-// path cannot occur): MF mass-flux instrumentation; FC manufactured
-// forcing; DIR Dirichlet ghosts; HBC hb_mode "const" terms.
-template <int k, bool MF = false, bool FC = true, bool DIR = true, bool HBC = true>
+// V: compile-time variant (V_* above)
+template <int k, int V = V_GENERAL>
 __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     stage_kernel(Tab T, Phys P, StageArgs A) {
   using O = Ord<k>;
@@ -823,7 +832,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 
   if constexpr (k <= 2) {
     if (QF_EN_VOL && (A.terms & TERM_VOL))
-      volume_terms<k, HBC>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
+      volume_terms<k, V>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
   } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
@@ -839,8 +848,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
       r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
     }
-    if (FC && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
-      forcing_quad<k>(P, T, e, t, B11, B12, B21, B22, sd,
+    if ((V & V_FC) && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
+      forcing_quad<k, V>(P, T, e, t, B11, B12, B21, B22, sd,
                       [&](const double* Pq, double S, double Fx, double Fy) {
 #pragma unroll
                         for (int p = 0; p < K; ++p) {
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #endif
     QF_UNROLL(QF_EUNROLL)
     for (int j = 0; j < QF_FAKE_NEDGE; ++j)  // (timing experiments only: < 3 is wrong numerics)
-      edge_term<k, Blk<k>::value, MF, DIR, HBC>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
+      edge_term<k, Blk<k>::value, V>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
   }
   if (A.mode == 0) {
@@ -1340,6 +1349,21 @@ __global__ void request_count_kernel(const int* __restrict__ nbr, int64_t ld, in
   if ((threadIdx.x & 31) == 0) atomicMax(out, c);
 }
 
+// 1 in *out if any owned element has a reflective-wall edge (boundary code
+// -1 - (2 slot + 1)): selects stage-kernel instances with the wall code
+__global__ void wall_scan_kernel(const int* __restrict__ nbr, int64_t ld, int n,
+                                 int* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  for (int j = 0; j < 3; ++j) {
+    const int code = nbr[j * ld + e];
+    if (code < 0 && ((-1 - code) & 1)) {
+      *out = 1;
+      return;
+    }
+  }
+}
+
 // ===================================================================== ABI
 using namespace qf;
 
@@ -1357,6 +1381,7 @@ struct qf_ctx {
   double* vol = nullptr;  // k >= 3 volume-rhs scratch [3K][ld] (context-owned)
   int hcap = QF_HCAP;     // stage-kernel request slots per block (measured in qf_create)
   double* l2part = nullptr;  // qf_l2_error block partials [3][blocks] (grown on demand)
+  bool walls = true;         // any reflective-wall boundary code in nbr (measured in qf_create)
   int l2cap = 0;
 };
 
@@ -1384,16 +1409,15 @@ static int cuda_check(const char* what) {
   }
 
 // one stage-kernel instance: the dynamic shared-memory opt-in once per instance
-template <int k, bool MF, bool FC, bool DIR, bool HBC>
+template <int k, int V>
 static void stage_inst(qf_ctx* x, const StageArgs& a, cudaStream_t s, int grid, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_kernel<k, MF, FC, DIR, HBC>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(stage_kernel<k, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)stage_smem_bytes<k>(QF_HCAP));
     attr = true;
   }
-  stage_kernel<k, MF, FC, DIR, HBC><<<grid, Blk<k>::value, smem, s>>>(x->tab, x->phys, a);
+  stage_kernel<k, V><<<grid, Blk<k>::value, smem, s>>>(x->tab, x->phys, a);
 }
 
 template <int k>
@@ -1425,18 +1449,38 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   const size_t smem = stage_smem_bytes<k>(a.hcap);
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
+  // the variant this problem needs, then the smallest compiled instance
+  // that covers it (instances: see the switch)
   const Phys& P = x->phys;
-  const bool lean = P.hb_linear && ((QF_LEAN_INST >> k) & 1);
-  if (a.mflux)  // instrumented instance (mass-flux diagnostics only)
-    stage_inst<k, true, true, true, true>(x, a, s, grid, smem);
-  else if (lean && P.forcing && x->d.n_bnd > 0)  // manufactured solutions (C1, C2)
-    stage_inst<k, false, true, true, false>(x, a, s, grid, smem);
-  else if (lean && !P.forcing && x->d.n_bnd == 0)  // walls, no forcing (C3-C5)
-    stage_inst<k, false, false, false, false>(x, a, s, grid, smem);
-  else if (!P.forcing && ((QF_NOFORCE_INST >> k) & 1))
-    stage_inst<k, false, false, true, true>(x, a, s, grid, smem);
-  else
-    stage_inst<k, false, true, true, true>(x, a, s, grid, smem);
+  int v = V_GENERAL;
+  if (a.mflux) {
+    v = V_MF | V_GENERAL;
+  } else if ((QF_LEAN_INST >> k) & 1) {
+    v = (P.forcing ? V_FC : 0) | (x->d.n_bnd > 0 ? V_DIR : 0) | (P.hb_linear ? 0 : V_HBC) |
+        (x->walls ? V_WALL : 0);
+    if (P.forcing && P.kind == SCN_MMS && P.taylor == 2) v |= V_TAY7;
+  } else if (!P.forcing && ((QF_NOFORCE_INST >> k) & 1)) {
+    v = V_DIR | V_HBC | V_WALL;
+  }
+  switch (v) {
+    case V_FC | V_DIR | V_TAY7:  // BASELINE MMS at small element size (C2)
+      stage_inst<k, V_FC | V_DIR | V_TAY7>(x, a, s, grid, smem);
+      break;
+    case V_FC | V_DIR:  // MMS / travelling wave, Dirichlet only (C1)
+      stage_inst<k, V_FC | V_DIR>(x, a, s, grid, smem);
+      break;
+    case V_WALL:  // reflective walls, no forcing (C3-C5)
+      stage_inst<k, V_WALL>(x, a, s, grid, smem);
+      break;
+    case V_DIR | V_HBC | V_WALL:
+      stage_inst<k, V_DIR | V_HBC | V_WALL>(x, a, s, grid, smem);
+      break;
+    case V_MF | V_GENERAL:
+      stage_inst<k, V_MF | V_GENERAL>(x, a, s, grid, smem);
+      break;
+    default:
+      stage_inst<k, V_GENERAL>(x, a, s, grid, smem);
+  }
   g_launches++;
   if constexpr (k >= QF_VSPLIT) {
     if (a.mode == 1) {
@@ -1548,6 +1592,15 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
     }
     const int wc = std::min(std::max((h + 3) / 4 * 4, 4), QF_HCAP / nw);
     x->hcap = wc * nw;
+    int w = 0;
+    wall_scan_kernel<<<(d->n_elem + 255) / 256, 256>>>(d->nbr, d->ld, d->n_elem, (int*)x->err);
+    if (cudaMemcpy(&w, x->err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemset(x->err, 0, sizeof(unsigned)) != cudaSuccess) {
+      cudaFree(x->err);
+      delete x;
+      return fail(QF_E_CUDA, "wall scan failed");
+    }
+    x->walls = w != 0;
   }
   *out = x;
   return QF_OK;
