@@ -200,7 +200,8 @@ enum : int {
   V_HBC = 8,    // hb_mode "const" terms
   V_WALL = 16,  // reflective walls
   V_TAY7 = 32,  // MMS forcing with degree-7 Taylor phases only (no generic forcing code)
-  V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL
+  V_OVF = 64,   // request-slot overflow path (in-loop gather of out-of-block neighbours)
+  V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL | V_OVF
 };
 
 // orders whose stage kernel also exchanges the static h_b edge traces through
@@ -270,12 +271,12 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
           const double v = s_tr[((jn * NF + f) * NT + a) * BS + ns];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
-    } else if (QF_NOFALLBACK || hslot >= 0) {  // out-of-block neighbour, traced in phase A2
+    } else if (QF_NOFALLBACK || !(V & V_OVF) || hslot >= 0) {  // out-of-block, traced in A2
 #pragma unroll
       for (int f = 0; f < NF; ++f)
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          const double v = s_ht[(f * NT + a) * HC + (QF_NOFALLBACK ? max(hslot, 0) : hslot)];
+          const double v = s_ht[(f * NT + a) * HC + hslot];
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
     } else {  // request list overflow (rare): gather and trace here, compact code
@@ -492,6 +493,12 @@ struct VGroups {
 // k = 1..4 2.5-3.5 % faster)
 #ifndef QF_LEAN_INST
 #define QF_LEAN_INST 30
+#endif
+// orders (bit mask) whose whole-mesh launches use instances without the
+// request-overflow path when it cannot trigger (k = 2: C2 53.5 -> 51.9 us,
+// walls 144 -> 136 us at N = 512; k = 3 -0.8 %; k = 1 and k = 4 slower)
+#ifndef QF_NOOVF_ORDERS
+#define QF_NOOVF_ORDERS 12
 #endif
 // input-outer volume kernel (k = 4): pressure rows from symmetric products
 // (vol_press; measured k = 4 stage 1007 -> 966 us at N = 512; the row-outer
@@ -1382,6 +1389,7 @@ struct qf_ctx {
   int hcap = QF_HCAP;     // stage-kernel request slots per block (measured in qf_create)
   double* l2part = nullptr;  // qf_l2_error block partials [3][blocks] (grown on demand)
   bool walls = true;         // any reflective-wall boundary code in nbr (measured in qf_create)
+  bool fits = false;         // busiest warp's requests fit hcap (whole-mesh launches never overflow)
   int l2cap = 0;
 };
 
@@ -1450,30 +1458,42 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   const int grid = (a.n + bs - 1) / bs;
   if (grid == 0) return;
   // the variant this problem needs, then the smallest compiled instance
-  // that covers it (instances: see the switch)
+  // that covers it (instances: see the switch).  The request-overflow path
+  // is compiled out only for whole-mesh launches whose busiest warp fits the
+  // request slots measured in qf_create (blocks then equal the measured ones).
   const Phys& P = x->phys;
+  const bool ovf = !(x->fits && a.e0 == 0 && a.n == x->d.n_elem && ((QF_NOOVF_ORDERS >> k) & 1));
   int v = V_GENERAL;
   if (a.mflux) {
     v = V_MF | V_GENERAL;
   } else if ((QF_LEAN_INST >> k) & 1) {
     v = (P.forcing ? V_FC : 0) | (x->d.n_bnd > 0 ? V_DIR : 0) | (P.hb_linear ? 0 : V_HBC) |
-        (x->walls ? V_WALL : 0);
+        (x->walls ? V_WALL : 0) | (ovf ? V_OVF : 0);
     if (P.forcing && P.kind == SCN_MMS && P.taylor == 2) v |= V_TAY7;
   } else if (!P.forcing && ((QF_NOFORCE_INST >> k) & 1)) {
-    v = V_DIR | V_HBC | V_WALL;
+    v = V_DIR | V_HBC | V_WALL | V_OVF;
   }
   switch (v) {
     case V_FC | V_DIR | V_TAY7:  // BASELINE MMS at small element size (C2)
       stage_inst<k, V_FC | V_DIR | V_TAY7>(x, a, s, grid, smem);
       break;
+    case V_FC | V_DIR | V_TAY7 | V_OVF:
+      stage_inst<k, V_FC | V_DIR | V_TAY7 | V_OVF>(x, a, s, grid, smem);
+      break;
     case V_FC | V_DIR:  // MMS / travelling wave, Dirichlet only (C1)
       stage_inst<k, V_FC | V_DIR>(x, a, s, grid, smem);
+      break;
+    case V_FC | V_DIR | V_OVF:
+      stage_inst<k, V_FC | V_DIR | V_OVF>(x, a, s, grid, smem);
       break;
     case V_WALL:  // reflective walls, no forcing (C3-C5)
       stage_inst<k, V_WALL>(x, a, s, grid, smem);
       break;
-    case V_DIR | V_HBC | V_WALL:
-      stage_inst<k, V_DIR | V_HBC | V_WALL>(x, a, s, grid, smem);
+    case V_WALL | V_OVF:  // (partition ranges)
+      stage_inst<k, V_WALL | V_OVF>(x, a, s, grid, smem);
+      break;
+    case V_DIR | V_HBC | V_WALL | V_OVF:
+      stage_inst<k, V_DIR | V_HBC | V_WALL | V_OVF>(x, a, s, grid, smem);
       break;
     case V_MF | V_GENERAL:
       stage_inst<k, V_MF | V_GENERAL>(x, a, s, grid, smem);
@@ -1592,6 +1612,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
     }
     const int wc = std::min(std::max((h + 3) / 4 * 4, 4), QF_HCAP / nw);
     x->hcap = wc * nw;
+    x->fits = h <= wc;
     int w = 0;
     wall_scan_kernel<<<(d->n_elem + 255) / 256, 256>>>(d->nbr, d->ld, d->n_elem, (int*)x->err);
     if (cudaMemcpy(&w, x->err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
