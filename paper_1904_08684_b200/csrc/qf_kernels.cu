@@ -497,6 +497,11 @@ struct VGroups {
 // orders (bit mask) whose whole-mesh launches use instances without the
 // request-overflow path when it cannot trigger (k = 2: C2 53.5 -> 51.9 us,
 // walls 144 -> 136 us at N = 512; k = 3 -0.8 %; k = 1 and k = 4 slower)
+// orders (bit mask) whose volume kernels drop the hb_mode "const" code for
+// linear h_b (k = 4: stage 944 -> 907 us at N = 512; k = 3: 355 -> 374, not used)
+#ifndef QF_VLEAN_ORDERS
+#define QF_VLEAN_ORDERS 16
+#endif
 #ifndef QF_NOOVF_ORDERS
 #define QF_NOOVF_ORDERS 12
 #endif
@@ -920,7 +925,7 @@ struct GRow {
 #ifndef QF_VOCC
 #define QF_VOCC 1
 #endif
-template <int k, int GRP = 0>
+template <int k, int GRP = 0, bool HBC = true>  // HBC: hb_mode "const" code compiled
 __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
                                                      const double* __restrict__ u, int e0, int n,
                                                      double* __restrict__ vol) {
@@ -943,7 +948,8 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] = 0.0;
-    volume_terms<k>(P, B11, B12, B21, B22, isd, idet, cc, cc + K, cc + 2 * K, uu, hb, r);
+    volume_terms<k, HBC ? V_GENERAL : 0>(P, B11, B12, B21, B22, isd, idet, cc, cc + K, cc + 2 * K,
+                                         uu, hb, r);
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) vol[i * ld + e] = r[i];
     return;
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     O::template vol_uv_acc<P0, P1>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12, g * B11,
                                    r + K, r + 2 * K);
   }
-  if (!P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+  if (HBC && !P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
     double xi[K], ra[K], rb[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) xi[i] = ldg(c + i * ld + e);
@@ -1026,7 +1032,7 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
   }
 }
 
-template <int k>
+template <int k, bool PUSH = false>  // PUSH: fused halo push compiled
 __global__ void __launch_bounds__(128)
     velocity_kernel(Tab T, const double* __restrict__ c, double* __restrict__ u, int e0, int n,
                     unsigned* err, const int* __restrict__ push = nullptr,
@@ -1053,7 +1059,7 @@ __global__ void __launch_bounds__(128)
     u[i * ld + e] = uo[i];
     u[(K + i) * ld + e] = vo[i];
   }
-  if (push) push_rows<K>(push, peers, ld, e, c, uo, vo);
+  if constexpr (PUSH) push_rows<K>(push, peers, ld, e, c, uo, vo);
 }
 
 // Dirichlet ghost data: exact (xi, U, V, u, v) at the k+2 Gauss points of
@@ -1428,6 +1434,25 @@ static void stage_inst(qf_ctx* x, const StageArgs& a, cudaStream_t s, int grid, 
   stage_kernel<k, V><<<grid, Blk<k>::value, smem, s>>>(x->tab, x->phys, a);
 }
 
+// one launch per output group (separate register allocation per group)
+template <int k, bool HBC>
+static void launch_volume(qf_ctx* x, const StageArgs& a, int vg, cudaStream_t s) {
+  volume_kernel<k, 0, HBC><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+  g_launches++;
+  if constexpr (VGroups<k>::value > 1) {
+    volume_kernel<k, 1, HBC><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+    g_launches++;
+  }
+  if constexpr (VGroups<k>::value > 2) {
+    volume_kernel<k, 2, HBC><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+    g_launches++;
+  }
+  if constexpr (VGroups<k>::value > 3) {
+    volume_kernel<k, 3, HBC><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
+    g_launches++;
+  }
+}
+
 template <int k>
 static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   StageArgs a = a_in;
@@ -1435,20 +1460,10 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
     if ((a.terms & TERM_VOL) && a.n > 0) {
       // one launch per input group (separate register allocation per group)
       const int vg = (a.n + 127) / 128;
-      volume_kernel<k, 0><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
-      g_launches++;
-      if constexpr (VGroups<k>::value > 1) {
-        volume_kernel<k, 1><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
-        g_launches++;
-      }
-      if constexpr (VGroups<k>::value > 2) {
-        volume_kernel<k, 2><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
-        g_launches++;
-      }
-      if constexpr (VGroups<k>::value > 3) {
-        volume_kernel<k, 3><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.u, a.e0, a.n, x->vol);
-        g_launches++;
-      }
+      if (x->phys.hb_linear && ((QF_VLEAN_ORDERS >> k) & 1))
+        launch_volume<k, false>(x, a, vg, s);
+      else
+        launch_volume<k, true>(x, a, vg, s);
       a.vol = x->vol;
     }
   }
@@ -1504,8 +1519,12 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   g_launches++;
   if constexpr (k >= QF_VSPLIT) {
     if (a.mode == 1) {
-      velocity_kernel<k><<<(a.n + 127) / 128, 128, 0, s>>>(x->tab, a.c_out, a.u_out, a.e0, a.n,
-                                                        x->err, a.push, a.peers);
+      if (a.push)
+        velocity_kernel<k, true><<<(a.n + 127) / 128, 128, 0, s>>>(
+            x->tab, a.c_out, a.u_out, a.e0, a.n, x->err, a.push, a.peers);
+      else
+        velocity_kernel<k><<<(a.n + 127) / 128, 128, 0, s>>>(x->tab, a.c_out, a.u_out, a.e0, a.n,
+                                                          x->err);
       g_launches++;
     }
   }
