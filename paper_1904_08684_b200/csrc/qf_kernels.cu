@@ -201,6 +201,7 @@ enum : int {
   V_WALL = 16,  // reflective walls
   V_TAY7 = 32,  // MMS forcing with degree-7 Taylor phases only (no generic forcing code)
   V_OVF = 64,   // request-slot overflow path (in-loop gather of out-of-block neighbours)
+  V_STG = 128,  // RK-stage launch only: all terms, mode 1, no lambda output
   V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL | V_OVF
 };
 
@@ -397,7 +398,7 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     hmin = sH[s] < hmin ? sH[s] : hmin;
   }
   if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
-  if (A.lam) A.lam[j * ld + e] = lam;
+  if (!(V & V_STG) && A.lam) A.lam[j * ld + e] = lam;
 
   // Lax-Friedrichs flux in trace space (reference solver.py:610-613)
   double wO[NT], wN[NT], pO[NT], pN[NT], aO[NT], aN[NT], bO[NT], bN[NT];
@@ -481,12 +482,6 @@ struct VGroups {
   static constexpr int value = k == 4 ? QF_VG4 : (k == 3 ? QF_VG3 : 1);
 };
 
-// orders (bit mask) whose scenarios without manufactured forcing launch a
-// stage-kernel instance without the forcing code (measured at N = 512:
-// k = 3 381 -> 370 us; k = 1, 2 slower, k = 4 equal)
-#ifndef QF_NOFORCE_INST
-#define QF_NOFORCE_INST 8
-#endif
 // orders (bit mask) that launch lean instances for hb_mode "linear": without
 // the constant-h_b code, and for wall-only, forcing-free problems also
 // without the Dirichlet-ghost and forcing code (measured at N = 512, walls:
@@ -674,7 +669,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   // trip, overlapped with the table copy below
   const double B11 = ldg(T.geo + ee), B12 = ldg(T.geo + ld + ee);
   const double B21 = ldg(T.geo + 2 * ld + ee), B22 = ldg(T.geo + 3 * ld + ee);
-  const bool edges = (A.terms & TERM_EDGE) != 0;
+  const bool edges = (V & V_STG) || (A.terms & TERM_EDGE) != 0;
   int code[3] = {0, 0, 0};
   // k <= 2: the element's own data is loaded once up front and stays in
   // registers; for k >= 3 (6K values) each phase re-reads it (L1/L2)
@@ -843,14 +838,14 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double* cV = c + 2 * K;
 
   if constexpr (k <= 2) {
-    if (QF_EN_VOL && (A.terms & TERM_VOL))
+    if (QF_EN_VOL && ((V & V_STG) || (A.terms & TERM_VOL)))
       volume_terms<k, V>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
   } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
 
   }
-  if (QF_EN_SRC && (A.terms & TERM_SRC)) {  // reference solver.py:708-725 (+ xi mass source)
+  if (QF_EN_SRC && ((V & V_STG) || (A.terms & TERM_SRC))) {  // solver.py:708-725 (+ xi mass source)
     double d1, d2;
     O::hb_dref(hb, d1, d2);
     const double i32 = idet * isd;
@@ -882,7 +877,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       edge_term<k, Blk<k>::value, V>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
   }
-  if (A.mode == 0) {
+  if (!(V & V_STG) && A.mode == 0) {
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) A.c_out[i * ld + e] = r[i];
     return;
@@ -1481,34 +1476,29 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   int v = V_GENERAL;
   if (a.mflux) {
     v = V_MF | V_GENERAL;
-  } else if ((QF_LEAN_INST >> k) & 1) {
+  } else if (a.mode == 1 && ((QF_LEAN_INST >> k) & 1)) {
     v = (P.forcing ? V_FC : 0) | (x->d.n_bnd > 0 ? V_DIR : 0) | (P.hb_linear ? 0 : V_HBC) |
-        (x->walls ? V_WALL : 0) | (ovf ? V_OVF : 0);
+        (x->walls ? V_WALL : 0) | (ovf ? V_OVF : 0) | V_STG;
     if (P.forcing && P.kind == SCN_MMS && P.taylor == 2) v |= V_TAY7;
-  } else if (!P.forcing && ((QF_NOFORCE_INST >> k) & 1)) {
-    v = V_DIR | V_HBC | V_WALL | V_OVF;
   }
   switch (v) {
-    case V_FC | V_DIR | V_TAY7:  // BASELINE MMS at small element size (C2)
-      stage_inst<k, V_FC | V_DIR | V_TAY7>(x, a, s, grid, smem);
+    case V_STG | V_FC | V_DIR | V_TAY7:  // BASELINE MMS at small element size (C2)
+      stage_inst<k, V_STG | V_FC | V_DIR | V_TAY7>(x, a, s, grid, smem);
       break;
-    case V_FC | V_DIR | V_TAY7 | V_OVF:
-      stage_inst<k, V_FC | V_DIR | V_TAY7 | V_OVF>(x, a, s, grid, smem);
+    case V_STG | V_FC | V_DIR | V_TAY7 | V_OVF:
+      stage_inst<k, V_STG | V_FC | V_DIR | V_TAY7 | V_OVF>(x, a, s, grid, smem);
       break;
-    case V_FC | V_DIR:  // MMS / travelling wave, Dirichlet only (C1)
-      stage_inst<k, V_FC | V_DIR>(x, a, s, grid, smem);
+    case V_STG | V_FC | V_DIR:  // MMS / travelling wave, Dirichlet only (C1)
+      stage_inst<k, V_STG | V_FC | V_DIR>(x, a, s, grid, smem);
       break;
-    case V_FC | V_DIR | V_OVF:
-      stage_inst<k, V_FC | V_DIR | V_OVF>(x, a, s, grid, smem);
+    case V_STG | V_FC | V_DIR | V_OVF:
+      stage_inst<k, V_STG | V_FC | V_DIR | V_OVF>(x, a, s, grid, smem);
       break;
-    case V_WALL:  // reflective walls, no forcing (C3-C5)
-      stage_inst<k, V_WALL>(x, a, s, grid, smem);
+    case V_STG | V_WALL:  // reflective walls, no forcing (C3-C5)
+      stage_inst<k, V_STG | V_WALL>(x, a, s, grid, smem);
       break;
-    case V_WALL | V_OVF:  // (partition ranges)
-      stage_inst<k, V_WALL | V_OVF>(x, a, s, grid, smem);
-      break;
-    case V_DIR | V_HBC | V_WALL | V_OVF:
-      stage_inst<k, V_DIR | V_HBC | V_WALL | V_OVF>(x, a, s, grid, smem);
+    case V_STG | V_WALL | V_OVF:  // (k = 1, 4 and partition ranges)
+      stage_inst<k, V_STG | V_WALL | V_OVF>(x, a, s, grid, smem);
       break;
     case V_MF | V_GENERAL:
       stage_inst<k, V_MF | V_GENERAL>(x, a, s, grid, smem);
