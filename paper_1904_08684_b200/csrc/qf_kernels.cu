@@ -202,7 +202,9 @@ enum : int {
   V_TAY7 = 32,  // MMS forcing with degree-7 Taylor phases only (no generic forcing code)
   V_OVF = 64,   // request-slot overflow path (in-loop gather of out-of-block neighbours)
   V_STG = 128,  // RK-stage launch only: all terms, mode 1, no lambda output
-  V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL | V_OVF
+  V_PUSH = 256, // fused halo push in the epilogue (k <= 2)
+  V_FRIC = 512, // bottom friction / Coriolis source terms
+  V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL | V_OVF | V_PUSH | V_FRIC
 };
 
 // orders whose stage kernel also exchanges the static h_b edge traces through
@@ -852,8 +854,13 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     const double gx = P.g * (B22 * d1 - B21 * d2) * i32, gy = P.g * (-B12 * d1 + B11 * d2) * i32;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
-      r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
+      if constexpr ((V & V_FRIC) != 0) {
+        r[K + i] += -P.tau * cU[i] + P.fc * cV[i] + gx * xi[i];
+        r[2 * K + i] += -P.tau * cV[i] - P.fc * cU[i] + gy * xi[i];
+      } else {  // tau = f_c = 0
+        r[K + i] += __dmul_rn(gx, xi[i]);
+        r[2 * K + i] += __dmul_rn(gy, xi[i]);
+      }
     }
     if ((V & V_FC) && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
       forcing_quad<k, V>(P, T, e, t, B11, B12, B21, B22, sd,
@@ -904,7 +911,9 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     A.u_out[i * ld + e] = uo[i];
     A.u_out[(K + i) * ld + e] = vo[i];
   }
-  if (A.push) push_rows<K>(A.push, A.peers, ld, e, A.c_out, uo, vo);
+  if constexpr ((V & V_PUSH) != 0) {
+    if (A.push) push_rows<K>(A.push, A.peers, ld, e, A.c_out, uo, vo);
+  }
 }
 
 // k >= 3: the volume contraction as its own launch (the fused stage kernel
@@ -1476,7 +1485,8 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   int v = V_GENERAL;
   if (a.mflux) {
     v = V_MF | V_GENERAL;
-  } else if (a.mode == 1 && ((QF_LEAN_INST >> k) & 1)) {
+  } else if (a.mode == 1 && !a.push && P.tau == 0.0 && P.fc == 0.0 &&
+             ((QF_LEAN_INST >> k) & 1)) {
     v = (P.forcing ? V_FC : 0) | (x->d.n_bnd > 0 ? V_DIR : 0) | (P.hb_linear ? 0 : V_HBC) |
         (x->walls ? V_WALL : 0) | (ovf ? V_OVF : 0) | V_STG;
     if (P.forcing && P.kind == SCN_MMS && P.taylor == 2) v |= V_TAY7;
