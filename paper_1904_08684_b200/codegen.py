@@ -393,14 +393,14 @@ def gen_order(k: int) -> str:
     # ---- tables for the looped (non-unrolled) edge and quadrature code:
     # Lam[3][K][NT] | QX[NQ] | QY[NQ] | P[NQ][K] (P = w_q phi_p(q)) | GS[NG] |
     # GPSI[NT][NG] (psi_a(s_g) w_g, Dirichlet ghost moments) | PHI[NQ][K] (phi_p(q)) |
-    # QW[NQ] (w_q, error quadrature)
+    # QW[NQ] (w_q, error quadrature) | QR1, QR2[NQ] (quadrature points minus the centroid)
     gpsi = np.array([[float(legendre01(a, gs[g])) * gw[g] for g in range(NG)] for a in range(NT)])
     # (entries the literal trace code skips are zeroed, so a table-driven
     # trace reproduces its bits)
     lam_t = np.where(np.abs(ts.Lam) > TOL, ts.Lam, 0.0)
     tab = list(lam_t.ravel()) + list(qp[:, 0]) + list(qp[:, 1]) + \
         list((phi_q * qw[None, :]).T.ravel()) + list(gs) + list(gpsi.ravel()) + \
-        list(phi_q.T.ravel()) + list(qw)
+        list(phi_q.T.ravel()) + list(qw) + list(qp[:, 0] - 1.0 / 3.0) + list(qp[:, 1] - 1.0 / 3.0)
     w(f"__constant__ double c_tab{k}[{len(tab)}] = {{")
     for i0 in range(0, len(tab), 4):
         w("  " + ", ".join(lit(v) for v in tab[i0:i0 + 4]) + ",")
@@ -410,7 +410,8 @@ def gen_order(k: int) -> str:
     o_gs = o_p + NQ * K
     w(f"  static constexpr int L = 0, QX = {3 * K * NT}, QY = {3 * K * NT + NQ}, P = {o_p}, "
       f"GS = {o_gs}, GPSI = {o_gs + NG}, PHI = {o_gs + NG + NT * NG}, "
-      f"QW = {o_gs + NG + NT * NG + NQ * K}, SIZE = {len(tab)};")
+      f"QW = {o_gs + NG + NT * NG + NQ * K}, QR1 = {o_gs + NG + NT * NG + NQ * K + NQ}, "
+      f"QR2 = {o_gs + NG + NT * NG + NQ * K + 2 * NQ}, SIZE = {len(tab)};")
     w(f"  static __device__ __forceinline__ const double* ptr() {{ return c_tab{k}; }}")
     w("};")
     w("}  // namespace qf")

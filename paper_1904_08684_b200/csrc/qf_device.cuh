@@ -41,11 +41,15 @@ struct Phys {
 
 // sin / cos of a small angle z (|z| <= 0.06): truncation < 1e-19 relative
 // |z| <= 0.02: remainders z^9/9! and z^8/8! are below 1e-18
+// (coefficients in the constant bank: DFMA operands instead of per-iteration
+// 64-bit immediates materialised by register moves)
+__constant__ double qf_taylor7[5] = {-1.984126984126984e-04, 8.333333333333333e-03,
+                                     -1.6666666666666666e-01, -1.388888888888889e-03,
+                                     4.1666666666666664e-02};
 __device__ __forceinline__ void sincos_small7(double z, double& s, double& c) {
   const double z2 = z * z;
-  s = z * fma(z2, fma(z2, fma(z2, -1.984126984126984e-04, 8.333333333333333e-03),
-                      -1.6666666666666666e-01), 1.0);
-  c = fma(z2, fma(z2, fma(z2, -1.388888888888889e-03, 4.1666666666666664e-02), -0.5), 1.0);
+  s = z * fma(z2, fma(z2, fma(z2, qf_taylor7[0], qf_taylor7[1]), qf_taylor7[2]), 1.0);
+  c = fma(z2, fma(z2, fma(z2, qf_taylor7[3], qf_taylor7[4]), -0.5), 1.0);
 }
 
 __device__ __forceinline__ void sincos_small(double z, double& s, double& c) {
@@ -123,6 +127,7 @@ __device__ __forceinline__ void flux_forcing(const Phys& P, double H, double Hx,
 //   Fx = u D + H (u_t + 2 u u_x + u v_y + g xi_x),
 //   Fy = v D + H (v_t + u_x v + 2 v v_y + g xi_y),   D = H_t + u H_x + v H_y,
 //   S  = xi_t + H_x u + H u_x + H_y v + H v_y   (u_y = v_x = 0).
+template <bool FRIC = true>  // FRIC: friction / Coriolis terms compiled (else tau = f_c = 0)
 __device__ __forceinline__ void forcing_mms(const Phys& P, double x, double y, double s1,
                                             double c1, double s2, double c2, double s3,
                                             double c3, double& S, double& Fx, double& Fy) {
@@ -136,7 +141,7 @@ __device__ __forceinline__ void forcing_mms(const Phys& P, double x, double y, d
   const double gxd = P.g * xd;
   Fx = fma(u, D, H * fma(u, fma(2.0, ux, vy), gxd - ux));
   Fy = fma(v, D, H * fma(v, fma(2.0, vy, ux), gxd - vy));
-  if (P.tau != 0.0 || P.fc != 0.0) {  // (adding the zero terms would not change the bits)
+  if (FRIC && (P.tau != 0.0 || P.fc != 0.0)) {  // (adding zero terms would not change the bits)
     Fx = Fx + P.tau * H * u - P.fc * H * v;
     Fy = Fy + P.tau * H * v + P.fc * H * u;
   }

@@ -607,23 +607,25 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
     sincospi(2.0 * (y0 - t), &sy0, &cy0);
     sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
   }
+  // per point: offsets (r1, r2) from the centroid (table), the physical point
+  // and the small phase angles 2 pi B r
+  const double t11 = TWO_PI * B11, t12 = TWO_PI * B12, t21 = TWO_PI * B21, t22 = TWO_PI * B22;
   QF_UNROLL(QF_QUNROLL)
   for (int q = 0; q < NQ; ++q) {
-    const double x1 = s_tab[TB::QX + q], x2 = s_tab[TB::QY + q];
-    const double x = a1x + B11 * x1 + B12 * x2, y = a1y + B21 * x1 + B22 * x2;
+    const double r1 = s_tab[TB::QR1 + q], r2 = s_tab[TB::QR2 + q];
+    const double x = fma(B11, r1, fma(B12, r2, x0)), y = fma(B21, r1, fma(B22, r2, y0));
     double S, Fx, Fy;
     if (tay) {
-      const double r1 = x1 - 1.0 / 3.0, r2 = x2 - 1.0 / 3.0;
       double sz, cz, sw, cw;
       if ((V & V_TAY7) || P.taylor == 2) {
-        sincos_small7(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-        sincos_small7(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+        sincos_small7(fma(t11, r1, t12 * r2), sz, cz);
+        sincos_small7(fma(t21, r1, t22 * r2), sw, cw);
       } else {
-        sincos_small(TWO_PI * (B11 * r1 + B12 * r2), sz, cz);
-        sincos_small(TWO_PI * (B21 * r1 + B22 * r2), sw, cw);
+        sincos_small(fma(t11, r1, t12 * r2), sz, cz);
+        sincos_small(fma(t21, r1, t22 * r2), sw, cw);
       }
       const double szw = fma(sz, cw, cz * sw), czw = fma(cz, cw, -sz * sw);
-      forcing_mms(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
+      forcing_mms<(V & V_FRIC) != 0>(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
                   fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
                   fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
     } else if constexpr (!(V & V_TAY7)) {
