@@ -484,23 +484,23 @@ struct VGroups {
   static constexpr int value = k == 4 ? QF_VG4 : (k == 3 ? QF_VG3 : 1);
 };
 
-// orders (bit mask) that launch lean instances for hb_mode "linear": without
-// the constant-h_b code, and for wall-only, forcing-free problems also
-// without the Dirichlet-ghost and forcing code (measured at N = 512, walls:
-// k = 1..4 2.5-3.5 % faster)
+// orders (bit mask) whose RK-stage launches use lean instances: only the
+// code paths the problem can take (forcing, Dirichlet, walls, const h_b,
+// friction; measured at N = 512, walls: k = 1..4 2.5-3.5 % faster; with the
+// stage-only V_STG: C2 51.6 -> 48.9 us, k = 2 walls 135 -> 125 us)
 #ifndef QF_LEAN_INST
 #define QF_LEAN_INST 30
 #endif
-// orders (bit mask) whose whole-mesh launches use instances without the
-// request-overflow path when it cannot trigger (k = 2: C2 53.5 -> 51.9 us,
-// walls 144 -> 136 us at N = 512; k = 3 -0.8 %; k = 1 and k = 4 slower)
 // orders (bit mask) whose volume kernels drop the hb_mode "const" code for
 // linear h_b (k = 4: stage 944 -> 907 us at N = 512; k = 3: 355 -> 374, not used)
 #ifndef QF_VLEAN_ORDERS
 #define QF_VLEAN_ORDERS 16
 #endif
+// orders (bit mask) whose whole-mesh launches use instances without the
+// request-overflow path when it cannot trigger (k = 2: C2 53.5 -> 51.9 us,
+// walls 144 -> 136 us at N = 512; k = 3 -0.8 %; k = 1 walls -1.5 %; k = 4 slower)
 #ifndef QF_NOOVF_ORDERS
-#define QF_NOOVF_ORDERS 12
+#define QF_NOOVF_ORDERS 14
 #endif
 // input-outer volume kernel (k = 4): pressure rows from symmetric products
 // (vol_press; measured k = 4 stage 1007 -> 966 us at N = 512; the row-outer
