@@ -44,11 +44,11 @@ CONFIGS = {
 # element (2 dfma + dmul + dadd, smsp__sass_thread_inst_executed_op_*), from
 # tools/kernel_counts.sh under ncu; summaries in profiles/r01_kernel_counts.txt
 PROFILED = {
-    "c1": {"bytes_per_elem": 292.1, "flop_per_elem": 3046.2},
-    "c2": {"bytes_per_elem": 479.9, "flop_per_elem": 5973.3},
-    "c3": {"bytes_per_elem": 2327.1, "flop_per_elem": 8453.9},
-    "c4": {"bytes_per_elem": 681.6, "flop_per_elem": 3333.3},
-    "c5": {"bytes_per_elem": 4140.9, "flop_per_elem": 18493.4},
+    "c1": {"bytes_per_elem": 288.2, "flop_per_elem": 3025.2},
+    "c2": {"bytes_per_elem": 479.9, "flop_per_elem": 5974.3},
+    "c3": {"bytes_per_elem": 2328.7, "flop_per_elem": 8391.9},
+    "c4": {"bytes_per_elem": 682.0, "flop_per_elem": 3289.3},
+    "c5": {"bytes_per_elem": 4162.9, "flop_per_elem": 18373.4},
 }
 # FP64 FMA-pipe peak of this B200, measured by tools/micro/fp64_pipes.cu
 # (DFMA 35.3 TF/s, DMMA 37.1 TF/s, one shared pipe; profiles/r01_fp64_pipes.txt)
