@@ -291,7 +291,7 @@ def gen_order(k: int) -> str:
     # U_p += g22 pi_1 - g21 pi_2, V_p += g11 pi_2 - g12 pi_1 (rows [P0, P1))
     # (generated for the orders whose volume kernel uses it only, so the
     # other orders' constant pools and register allocation are unchanged)
-    if k >= PRESS_MINK:
+    if k >= min(PRESS_MINK, MMA_MINK):
         _gen_press(w, rt, K, NH)
     # ---- traces and lifts
     for j in range(3):
@@ -414,8 +414,92 @@ def gen_order(k: int) -> str:
       f"QR2 = {o_gs + NG + NT * NG + NQ * K + 2 * NQ}, SIZE = {len(tab)};")
     w(f"  static __device__ __forceinline__ const double* ptr() {{ return c_tab{k}; }}")
     w("};")
+    if k >= MMA_MINK:
+        L.extend(_gen_mma(k, rt, K))
     w("}  // namespace qf")
     return "\n".join(L) + "\n"
+
+
+# orders whose volume advection Z[p,i] = sum_m T1[p,i,m] a_m + T2[p,i,m] b_m
+# runs on the FP64 tensor cores (mma.sync.m8n8k4.f64, vol_mma_kernel)
+MMA_MINK = 3
+MMA_PREFETCH = int(__import__("os").environ.get("QF_MMA_PREFETCH", "4"))
+
+
+def mma_layout(k: int, rt=None):
+    """Fragment plan of the FP64-MMA volume advection for order k.
+
+    GEMM per element tile of 8: D[el, n] = sum_kk A[el, kk] B[kk, n] with
+    A[el, kk] = (a; b)_kk of element el (kk = l K + m, l = 0: a_m, 1: b_m),
+    B[kk, n] = T[l, p, 8 ch + n, m] for output row p and input chunk ch, so
+    D[el, n] = Z_el[p, 8 ch + n].  Returns (NKS, frags) with frags a list of
+    (p, ch, s, values[32]) -- the m8n8k4 B fragment of k-step s, lane-major
+    (lane holds B[lane % 4][lane // 4]) -- all-zero fragments dropped."""
+    rt = rt or build_ref_tensors(k)
+    T = rt.T
+    K = T.shape[1]
+    nks = (2 * K + 3) // 4
+    nch = (K + 7) // 8
+    frags = []
+    for p in range(K):
+        for ch in range(nch):
+            for s in range(nks):
+                vals = []
+                for lane in range(32):
+                    kk, i = 4 * s + lane % 4, 8 * ch + lane // 4
+                    v = float(T[kk // K, p, i, kk % K]) if (kk < 2 * K and i < K) else 0.0
+                    vals.append(v if _nz(v) else 0.0)
+                if any(v != 0.0 for v in vals):
+                    frags.append((p, ch, s, vals))
+    return nks, frags
+
+
+def _gen_mma(k: int, rt, K: int) -> list:
+    nks, frags = mma_layout(k, rt)
+    nch = (K + 7) // 8
+    L = [f"// FP64 tensor-core volume advection, order {k}: {len(frags)} nonzero m8n8k4 B fragments",
+         f"// (of {K * nch * nks}), {nks} k-steps over (a; b), {nch} input chunks of 8 (codegen.mma_layout)",
+         f"__device__ const double qf_vmma{k}[{len(frags) * 32}] = {{"]
+    for (_, _, _, vals) in frags:
+        for i0 in range(0, 32, 4):
+            L.append("  " + ", ".join(lit(v) for v in vals[i0:i0 + 4]) + ",")
+    L.append("};")
+    L.append(f"template <> struct Mma<{k}> {{")
+    L.append(f"  static constexpr int K = {K}, NKS = {nks}, NCH = {nch}, NF = {len(frags)};")
+    L.append(f"  static __device__ __forceinline__ const double* table() {{ return qf_vmma{k}; }}")
+    L.append("  // pu[t][p] += sum_i Z_t[p,i] cu[t][i-slot] (likewise pv): sB = the fragment table in")
+    L.append("  // shared memory, A[t][s] = this lane's (a; b) entry of k-step s for tile t,")
+    L.append("  // cu/cv[t][2 ch + j] = c_U/c_V of input 8 ch + 2 (lane % 4) + j of the lane's element")
+    L.append("  template <int NT> static __device__ __forceinline__ void adv(const double* sB, int lane,")
+    L.append("      const double (&A)[NT][NKS], const double (&cu)[NT][2 * NCH], const double (&cv)[NT][2 * NCH],")
+    L.append("      double (&pu)[NT][K], double (&pv)[NT][K]) {")
+    # flat fragment order; the B fragment of step j + MMA_PREFETCH is loaded
+    # while step j multiplies (volatile shared loads and MMAs keep this
+    # order, so ptxas cannot hoist all NF loads and spill)
+    seq = [(f, p, ch, s_) for f, (p, ch, s_, _) in enumerate(frags)]
+    D = MMA_PREFETCH
+    L.append(f"    double bq[{D}];")
+    for j in range(min(D, len(seq))):
+        L.append(f"    bq[{j}] = lds64(sB + {seq[j][0] * 32} + lane);")
+    L.append("    double d0[NT], d1[NT];")
+    for j, (f, p, ch, s_) in enumerate(seq):
+        first = j == 0 or (seq[j - 1][1], seq[j - 1][2]) != (p, ch)
+        last = j + 1 == len(seq) or (seq[j + 1][1], seq[j + 1][2]) != (p, ch)
+        if first:
+            L.append("    #pragma unroll")
+            L.append("    for (int t = 0; t < NT; ++t) { d0[t] = 0.0; d1[t] = 0.0; }")
+        L.append(f"    {{ const double b = bq[{j % D}];")
+        if j + D < len(seq):
+            L.append(f"      bq[{j % D}] = lds64(sB + {seq[j + D][0] * 32} + lane);")
+        L.append("      #pragma unroll")
+        L.append(f"      for (int t = 0; t < NT; ++t) dmma(d0[t], d1[t], A[t][{s_}], b); }}")
+        if last:
+            L.append("    #pragma unroll")
+            L.append(f"    for (int t = 0; t < NT; ++t) {{ pu[t][{p}] = fma(d1[t], cu[t][{2 * ch + 1}], fma(d0[t], cu[t][{2 * ch}], pu[t][{p}]));"
+                     f" pv[t][{p}] = fma(d1[t], cv[t][{2 * ch + 1}], fma(d0[t], cv[t][{2 * ch}], pv[t][{p}])); }}")
+    L.append("  }")
+    L.append("};")
+    return L
 
 
 def generate(out_dir: Path = GEN_DIR, orders=range(MAX_ORDER + 1)) -> list[Path]:

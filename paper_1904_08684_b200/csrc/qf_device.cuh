@@ -14,6 +14,25 @@ template <int k>
 struct Ord;
 template <int k>
 struct Tabs;
+template <int k>
+struct Mma;  // FP64 tensor-core volume advection (generated for k >= 3)
+
+// shared-memory load kept in program order with the MMAs (see Mma<k>::adv)
+__device__ __forceinline__ double lds64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];"
+               : "=d"(v)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+// D = A B + C for one m8n8k4 FP64 tile (a, b: this lane's fragments; d0/d1:
+// the lane's two accumulators, updated in place)
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 constexpr double TWO_PI = 6.283185307179586;
 

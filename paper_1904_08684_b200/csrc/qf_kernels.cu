@@ -928,6 +928,29 @@ struct GRow {
   __device__ __forceinline__ double operator[](int i) const { return s * ldv(p + i * ld); }
 };
 
+// a row of the block's shared-memory copy of c (stride = block size)
+struct SRow {
+  const double* p;
+  double s;
+  __device__ __forceinline__ double operator[](int i) const { return s * p[i * 128]; }
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// k >= 4: the volume kernel copies its element's 3K state rows into shared
+// memory with one burst of cp.async (no registers held, every load in flight
+// at once) instead of the generated code's in-loop global loads (ncu: long
+// scoreboard was the top stall at 2 warps per scheduler)
+#ifndef QF_VSMEM
+#define QF_VSMEM 1
+#endif
+
 #ifndef QF_VOCC
 #define QF_VOCC 1
 #endif
@@ -966,6 +989,12 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
   constexpr int P1 = VG == 1 ? K : (VG == 2 ? O::VOL_PSPLIT2[grp + 1]
                                             : (VG == 3 ? O::VOL_PSPLIT3[grp + 1]
                                                        : O::VOL_PSPLIT4[grp + 1]));
+  constexpr bool SM = QF_VSMEM && k >= 4;
+  __shared__ double vsm[SM ? 3 * K * 128 : 1];
+  if constexpr (SM) {
+#pragma unroll
+    for (int i = 0; i < 3 * K; ++i) cp_async8(vsm + i * 128 + threadIdx.x, c + i * ld + e);
+  }
   double r[3 * K], al[K], be[K], wv[K];
   {  // xi row and the U/V operands a, b, w
     double cU[K], cV[K];
@@ -989,7 +1018,23 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
     }
   }
   const GRow gU{c + K * ld + e, ld, i32}, gV{c + 2 * K * ld + e, ld, i32}, gX{c + e, ld, i32};
-  if constexpr (QF_VPRESS && k >= 4) {  // advection part, then symmetric-product pressure rows
+  if constexpr (SM) {  // advection part from the shared copy, then symmetric-product pressure rows
+    cp_async_wait_all();
+    const double* sc = vsm + threadIdx.x;
+    const SRow sU{sc + K * 128, i32}, sV{sc + 2 * K * 128, i32}, sX{sc, i32};
+    O::template vol_uv_acc<P0, P1, !QF_VPRESS>(sU, sV, sX, al, be, wv, g * B22, g * B21, g * B12,
+                                               g * B11, r + K, r + 2 * K);
+    if constexpr (QF_VPRESS) {
+      double xi[K], hb[NH];
+#pragma unroll
+      for (int i = 0; i < K; ++i) xi[i] = sc[i * 128];
+#pragma unroll
+      for (int i = 0; i < NH; ++i) hb[i] = ldg(T.hb + i * ld + e);
+      const double gs = g * i32;
+      O::template vol_press<P0, P1>(xi, hb, P.hb_linear != 0, gs * B22, gs * B21, gs * B12,
+                                    gs * B11, r + K, r + 2 * K);
+    }
+  } else if constexpr (QF_VPRESS && k >= 4) {  // advection part, then symmetric-product pressure rows
     O::template vol_uv_acc<P0, P1, false>(gU, gV, gX, al, be, wv, g * B22, g * B21, g * B12,
                                           g * B11, r + K, r + 2 * K);
     double xi[K], hb[NH];
@@ -1035,6 +1080,177 @@ __global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, con
   for (int i = P0; i < P1; ++i) {
     vol[(K + i) * ld + e] = r[K + i];
     vol[(2 * K + i) * ld + e] = r[2 * K + i];
+  }
+}
+
+// k >= 3 with QF_VMMA: the volume rows in two launches.
+// volume_rest_kernel: xi row (vol_xi) and the pressure rows (vol_press,
+// symmetric products) -- thread per element, plain FP64;
+// vol_mma_kernel: the advection part of the U/V rows,
+//   U_p += sum_i Z[p,i] c_U,i / (detB sqrt(detB)),  Z[p,i] = sum_m T1[p,i,m] a_m + T2[p,i,m] b_m
+// (solver.py:459-482 factorised), as a GEMM on the FP64
+// tensor cores: per tile of 8 elements D[el, (p, i)] = (a; b)[el, :] . T[:, (p, i)]
+// with mma.sync.m8n8k4.f64 (the B fragments of T are the generated table
+// Mma<k>::table(), all-zero fragments dropped), then the contraction with
+// c_U / c_V in the accumulator registers and a quad reduction.  ncu on the
+// thread-per-element kernel: 2 warps per scheduler at 255 registers, FP64
+// pipe ~35 % busy on FFMA chains; one DMMA carries 256 multiply-adds.
+// Measured (N = 512, bumps + walls): k = 4 stage 901 -> 1057 us, k = 3 352 ->
+// 506 us.  vol_mma_kernel<4> 330 us with the DMMA pipe 54 % busy (long
+// scoreboard: per-tile operand loads) + volume_rest_kernel 196..325 us, against
+// ~480 us for the FFMA input-outer kernel pair: the contraction is bilinear in
+// the element data, so the tensor cores only take the first (linear) half and
+// the operand setup, pressure rows and an extra pass over the rows stay on
+// the FP64 pipe they share with DMMA.  Off by default (opt-in experiment).
+#ifndef QF_VMMA
+#define QF_VMMA 0  // bit mask of orders (k = 3: 8, k = 4: 16)
+#endif
+#ifndef QF_VMMA_BPS
+#define QF_VMMA_BPS 4  // resident vol_mma blocks per SM (persistent grid)
+#endif
+template <int k, bool HBC, bool ADD>  // ADD: U/V rows start from vol (vol_mma_kernel's advection)
+__global__ void __launch_bounds__(128) volume_rest_kernel(Tab T, Phys P, const double* __restrict__ c,
+                                                          int e0, int n, double* __restrict__ vol) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NH = O::NH;
+  const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e0 + n) return;
+  const int64_t ld = T.ld;
+  const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
+  const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
+  const double det = det2(B11, B12, B21, B22), isd = rsqrt_fast(det), idet = isd * isd;
+  const double i32 = idet * isd, g = P.g;
+  double r[3 * K], xi[K], hb[NH];
+  {
+    double al[K], be[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const double cU = ldg(c + (K + i) * ld + e), cV = ldg(c + (2 * K + i) * ld + e);
+      al[i] = B22 * cU - B12 * cV;
+      be[i] = -B21 * cU + B11 * cV;
+    }
+    O::vol_xi(al, be, r);
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    r[i] *= idet;
+    r[K + i] = 0.0;
+    r[2 * K + i] = 0.0;
+    xi[i] = ldg(c + i * ld + e);
+  }
+#pragma unroll
+  for (int i = 0; i < NH; ++i) hb[i] = ldg(T.hb + i * ld + e);
+  const double gs = g * i32;
+  O::template vol_press<0, K>(xi, hb, P.hb_linear != 0, gs * B22, gs * B21, gs * B12, gs * B11,
+                              r + K, r + 2 * K);
+  if (HBC && !P.hb_linear) {  // paper-form constant h_b (solver.py:498-510)
+    double al[K], be[K], ra[K], rb[K];
+    const double ghb = g * hb[0] * isd * 0.7071067811865476 * idet;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = B22 * xi[i];
+      be[i] = -B21 * xi[i];
+    }
+    O::vol_xi(al, be, ra);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      al[i] = -B12 * xi[i];
+      be[i] = B11 * xi[i];
+    }
+    O::vol_xi(al, be, rb);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      r[K + i] += ghb * ra[i];
+      r[2 * K + i] += ghb * rb[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3 * K; ++i) vol[i * ld + e] = (ADD && i >= K) ? vol[i * ld + e] + r[i] : r[i];
+}
+
+template <int k>
+struct MmaIn {  // raw loads of one element tile (prefetched one iteration ahead)
+  static constexpr int NKS = Mma<k>::NKS, NCH = Mma<k>::NCH;
+  double b11, b12, b21, b22, uu[NKS], uv[NKS], cu[2 * NCH], cv[2 * NCH];
+  __device__ __forceinline__ void load(const Tab& T, const double* __restrict__ c,
+                                       const double* __restrict__ u, int e, int q) {
+    constexpr int K = Mma<k>::K;
+    const int64_t ld = T.ld;
+    b11 = ldg(T.geo + e);
+    b12 = ldg(T.geo + ld + e);
+    b21 = ldg(T.geo + 2 * ld + e);
+    b22 = ldg(T.geo + 3 * ld + e);
+#pragma unroll
+    for (int s = 0; s < NKS; ++s) {  // (a; b)[4 s + q] needs u_m, v_m, m = (4 s + q) mod K
+      const int kk = 4 * s + q, m = kk >= K ? kk - K : kk;
+      uu[s] = kk < 2 * K ? ldg(u + m * ld + e) : 0.0;
+      uv[s] = kk < 2 * K ? ldg(u + (K + m) * ld + e) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * NCH; ++j) {  // inputs 8 ch + 2 q + (j & 1)
+      const int i = 8 * (j >> 1) + 2 * q + (j & 1);
+      cu[j] = i < K ? ldg(c + (K + i) * ld + e) : 0.0;
+      cv[j] = i < K ? ldg(c + (2 * K + i) * ld + e) : 0.0;
+    }
+  }
+};
+
+// writes the advection part of the U/V rows [K, 3K) of vol (volume_rest_kernel<k, .., true>
+// then adds the xi row and the pressure)
+#ifndef QF_VMMA_MINB
+#define QF_VMMA_MINB 3
+#endif
+template <int k>
+__global__ void __launch_bounds__(128, QF_VMMA_MINB) vol_mma_kernel(Tab T, const double* __restrict__ c,
+                                                      const double* __restrict__ u, int e0, int n,
+                                                      double* __restrict__ vol) {
+  using M = Mma<k>;
+  constexpr int K = M::K, NKS = M::NKS, NCH = M::NCH, NT = 1;
+  extern __shared__ double sB[];
+  for (int i = threadIdx.x; i < M::NF * 32; i += blockDim.x) sB[i] = M::table()[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, q = lane & 3, row = lane >> 2;
+  const int64_t ld = T.ld;
+  const int ngrp = (n + 7) / 8, stride = gridDim.x * 4;
+  int grp = blockIdx.x * 4 + (threadIdx.x >> 5);
+  auto elem = [&](int g) { const int loc = g * 8 + row; return e0 + (loc < n ? loc : n - 1); };
+  MmaIn<k> nx;
+  if (grp < ngrp) nx.load(T, c, u, elem(grp), q);
+  for (; grp < ngrp; grp += stride) {
+    const MmaIn<k> in = nx;
+    const int e = elem(grp);
+    if (grp + stride < ngrp) nx.load(T, c, u, elem(grp + stride), q);
+    const double det = det2(in.b11, in.b12, in.b21, in.b22), isd = rsqrt_fast(det);
+    const double i32 = isd * isd * isd;
+    double A[NT][NKS], cu[NT][2 * NCH], cv[NT][2 * NCH], pu[NT][K], pv[NT][K];
+#pragma unroll
+    for (int s = 0; s < NKS; ++s)  // a = B22 u - B12 v, b = -B21 u + B11 v
+      A[0][s] = 4 * s + q < K ? in.b22 * in.uu[s] - in.b12 * in.uv[s]
+                              : -in.b21 * in.uu[s] + in.b11 * in.uv[s];
+#pragma unroll
+    for (int j = 0; j < 2 * NCH; ++j) {
+      cu[0][j] = i32 * in.cu[j];
+      cv[0][j] = i32 * in.cv[j];
+    }
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      pu[0][p] = 0.0;
+      pv[0][p] = 0.0;
+    }
+    M::template adv<NT>(sB, lane, A, cu, cv, pu, pv);
+    const bool live = grp * 8 + row < n;
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      double su = pu[0][p], sv = pv[0][p];
+      su += __shfl_xor_sync(0xffffffffu, su, 1);
+      sv += __shfl_xor_sync(0xffffffffu, sv, 1);
+      su += __shfl_xor_sync(0xffffffffu, su, 2);
+      sv += __shfl_xor_sync(0xffffffffu, sv, 2);
+      if (live && (p & 3) == q) {
+        vol[(K + p) * ld + e] = su;
+        vol[(2 * K + p) * ld + e] = sv;
+      }
+    }
   }
 }
 
@@ -1392,6 +1608,7 @@ struct qf_ctx {
   Phys phys;
   unsigned* err;  // device error word
   int K, NT, block;
+  int n_sm = 148;  // multiprocessors of the context's device (persistent grids)
   // cached run graph
   cudaGraphExec_t graph = nullptr;
   const void* gkey[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -1466,10 +1683,22 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
     if ((a.terms & TERM_VOL) && a.n > 0) {
       // one launch per input group (separate register allocation per group)
       const int vg = (a.n + 127) / 128;
-      if (x->phys.hb_linear && ((QF_VLEAN_ORDERS >> k) & 1))
-        launch_volume<k, false>(x, a, vg, s);
-      else
-        launch_volume<k, true>(x, a, vg, s);
+      if constexpr (((QF_VMMA >> k) & 1) != 0) {
+        const int ngrp = (a.n + 7) / 8;
+        const int mg = std::min((ngrp + 3) / 4, x->n_sm * QF_VMMA_BPS);
+        vol_mma_kernel<k><<<mg, 128, Mma<k>::NF * 32 * sizeof(double), s>>>(x->tab, a.c, a.u, a.e0,
+                                                                           a.n, x->vol);
+        if (x->phys.hb_linear)
+          volume_rest_kernel<k, false, true><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.e0, a.n, x->vol);
+        else
+          volume_rest_kernel<k, true, true><<<vg, 128, 0, s>>>(x->tab, x->phys, a.c, a.e0, a.n, x->vol);
+        g_launches += 2;
+      } else {
+        if (x->phys.hb_linear && ((QF_VLEAN_ORDERS >> k) & 1))
+          launch_volume<k, false>(x, a, vg, s);
+        else
+          launch_volume<k, true>(x, a, vg, s);
+      }
       a.vol = x->vol;
     }
   }
@@ -1592,6 +1821,12 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
   qf_ctx* x = new qf_ctx();
   x->d = *d;
   x->K = (d->order + 1) * (d->order + 2) / 2;
+  {
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      x->n_sm = nsm;
+  }
   x->NT = d->order + 1;
   x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->hbt, d->ld, d->n_bnd};
   x->phys.g = d->g;
