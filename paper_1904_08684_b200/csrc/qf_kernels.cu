@@ -951,11 +951,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #define QF_VSMEM 1
 #endif
 
+// minimum resident volume_kernel blocks per SM (register cap): k = 4 with 3
+// (168 registers) 902 -> 875 us/stage at N = 512; k = 3 with 3: 352 -> 392 us
 #ifndef QF_VOCC
 #define QF_VOCC 1
 #endif
+#ifndef QF_VOCC4
+#define QF_VOCC4 3
+#endif
 template <int k, int GRP = 0, bool HBC = true>  // HBC: hb_mode "const" code compiled
-__global__ void __launch_bounds__(128, QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
+__global__ void __launch_bounds__(128, k == 4 ? QF_VOCC4 : QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
                                                      const double* __restrict__ u, int e0, int n,
                                                      double* __restrict__ vol) {
   using O = Ord<k>;
@@ -1254,8 +1259,11 @@ __global__ void __launch_bounds__(128, QF_VMMA_MINB) vol_mma_kernel(Tab T, const
   }
 }
 
+#ifndef QF_VELOCC4
+#define QF_VELOCC4 1
+#endif
 template <int k, bool PUSH = false>  // PUSH: fused halo push compiled
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : 1)
     velocity_kernel(Tab T, const double* __restrict__ c, double* __restrict__ u, int e0, int n,
                     unsigned* err, const int* __restrict__ push = nullptr,
                     const qf_peer* __restrict__ peers = nullptr) {
