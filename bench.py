@@ -465,6 +465,14 @@ def measure_e2e(disc, st0, steps):
         st = disc.step(State(st.c, st.u, st.t))
         _ = st.c
     api = time.perf_counter() - t0
+    # the whole-run public API: Discretization.run(numpy State, t_end) -- one
+    # upload of c, n_pipe graph-replayed steps, the error word read once, one
+    # download of the final State (c and u), wall clock
+    t_end = st0.t + n_pipe * disc.dt
+    _ = disc.run(State(st0.c.copy(), st0.u.copy(), st0.t), t_end=t_end).c
+    t0 = time.perf_counter()
+    _ = disc.run(State(st0.c.copy(), st0.u.copy(), st0.t), t_end=t_end).c
+    run_s = time.perf_counter() - t0
     return {"value": dof * n_pipe / (ms_pipe * 1e-3), "unit": "DoF-updates/s",
             "h2d_bytes_per_step": 8 * 3 * K * E, "d2h_bytes_per_step": 8 * 3 * K * E,
             "timing": "C ABI with pinned host State buffers, every step: H2D c, qf_pack, "
@@ -474,7 +482,12 @@ def measure_e2e(disc, st0, steps):
                        "d2h_bytes_per_step": 8 * 5 * K * E,
                        "timing": "same sequence on one stream, D2H of c and u, per-step events"},
             "public_api": {"value": dof * steps / api, "unit": "DoF-updates/s",
-                           "timing": "Discretization.step with numpy States, wall clock"}}
+                           "timing": "Discretization.step with numpy States, wall clock"},
+            "run_api": {"value": dof * n_pipe / run_s, "unit": "DoF-updates/s", "steps": n_pipe,
+                        "h2d_bytes_per_run": 8 * 3 * K * E, "d2h_bytes_per_run": 8 * 5 * K * E,
+                        "timing": "Discretization.run(numpy State, t_end) over the steps: one "
+                                  "upload of c, graph-replayed steps, error word read once, "
+                                  "one download of c and u, wall clock"}}
 
 
 def main():
