@@ -1262,8 +1262,11 @@ __global__ void __launch_bounds__(128, QF_VMMA_MINB) vol_mma_kernel(Tab T, const
 #ifndef QF_VELOCC4
 #define QF_VELOCC4 1
 #endif
+#ifndef QF_VELOCC3
+#define QF_VELOCC3 3  // k = 3 velocity at 168 registers: 358 -> 350 us/stage (N = 512)
+#endif
 template <int k, bool PUSH = false>  // PUSH: fused halo push compiled
-__global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : 1)
+__global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : (k == 3 ? QF_VELOCC3 : 1))
     velocity_kernel(Tab T, const double* __restrict__ c, double* __restrict__ u, int e0, int n,
                     unsigned* err, const int* __restrict__ push = nullptr,
                     const qf_peer* __restrict__ peers = nullptr) {
