@@ -73,6 +73,11 @@ typedef struct qf_desc {
                                <= 0.02, so the forcing may use element-local Taylor sin/cos of
                                degree 9 resp. 7 (truncation < 1e-18); 0 = libm sincospi */
   int32_t block;            /* threads per block (0 = default) */
+  const double* uni;        /* MMS, k <= 2: phase-offset table when the element Jacobians take at
+                               most two values (uniform split-square meshes), else NULL; layout:
+                               [0..3] class-1 B, then per class c (offset 8 + c*(6*NQ+2)) and
+                               quadrature point q: sin z, cos z, sin w, cos w, sin(z+w), cos(z+w)
+                               with (z, w) = 2 pi B (r_q - centroid), NQ = (k+2)^2 */
 } qf_desc;
 
 typedef struct qf_ctx qf_ctx;

@@ -36,6 +36,7 @@ class QfDesc(C.Structure):
         ("g", C.c_double), ("f_c", C.c_double), ("tau_bf", C.c_double),
         ("hb_linear", C.c_int32), ("scn_kind", C.c_int32), ("scn_params", C.c_double * 8),
         ("has_forcing", C.c_int32), ("taylor", C.c_int32), ("block", C.c_int32),
+        ("uni", C.c_void_p),
     ]
 
 

@@ -49,7 +49,17 @@ struct Tab {
   const double* __restrict__ hbt;    // [3*NT+1][ld] static h_b traces (qf_static)
   int64_t ld;
   int n_bnd;
+  // MMS phase-offset table of a mesh whose element Jacobians take at most
+  // two values (uniform split-square meshes), or null; layout UniTab below
+  const double* __restrict__ uni;
 };
+
+// uni table: [0..3] the Jacobian B of class 1 (every other element is
+// class 0), [8 + c*(6*NQ+2) + 6*q + 0..5] sin z, cos z, sin w, cos w,
+// sin(z+w), cos(z+w) of the class-c phase offsets z = 2 pi (B r_q)_x,
+// w = 2 pi (B r_q)_y at quadrature point q (r_q minus the centroid); the
+// 2-double pad puts the two class rows in different shared-memory banks
+__host__ __device__ constexpr int uni_size(int nq) { return 8 + 2 * (6 * nq + 2); }
 
 struct Phys {
   double g, fc, tau;

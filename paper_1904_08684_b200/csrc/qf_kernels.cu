@@ -204,6 +204,7 @@ enum : int {
   V_STG = 128,  // RK-stage launch only: all terms, mode 1, no lambda output
   V_PUSH = 256, // fused halo push in the epilogue (k <= 2)
   V_FRIC = 512, // bottom friction / Coriolis source terms
+  V_UNI = 1024, // MMS forcing with tabulated phase offsets only (Tab::uni, k <= 2)
   V_GENERAL = V_FC | V_DIR | V_HBC | V_WALL | V_OVF | V_PUSH | V_FRIC
 };
 
@@ -586,7 +587,7 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
 template <int k, int V = V_GENERAL, class Sink>
 __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e, double t,
                                              double B11, double B12, double B21, double B22,
-                                             double sd, Sink&& sink) {
+                                             double sd, const double* su, Sink&& sink) {
   using TB = Tabs<k>;
   constexpr int K = Ord<k>::K, NQ = Ord<k>::NQ;
   const int64_t ld = T.ld;
@@ -594,15 +595,20 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
   const double a1x = ldg(T.geo + 4 * ld + e), a1y = ldg(T.geo + 5 * ld + e);
   double st, ct;
   sincospi(2.0 * t, &st, &ct);
-  // MMS with small elements: sin/cos(2 pi x_q) = rotation of the centroid
-  // value by a Taylor-evaluated small angle (2 sincospi per element
-  // instead of 2 per quadrature point)
-  const bool tay = (V & V_TAY7) || (P.kind == SCN_MMS && P.taylor);
+  // MMS: sin/cos(2 pi x_q) = rotation of the centroid value by the small
+  // offset angle of point q, either read from the per-mesh table (su: the
+  // Jacobian takes at most two values, shared memory) or Taylor-evaluated
+  // (2 sincospi per element instead of 2 per quadrature point)
+  const bool uni = (V & V_UNI) ? true : (!(V & V_TAY7) && k <= 2 && su != nullptr && P.kind == SCN_MMS);
+  const bool tay = !uni && ((V & V_TAY7) || (P.kind == SCN_MMS && P.taylor));
+  const double* su_e = nullptr;
+  if (uni)
+    su_e = su + 8 + ((B11 == su[0] && B12 == su[1] && B21 == su[2] && B22 == su[3]) ? 6 * NQ + 2 : 0);
   // element phases 2 pi (x0 - t), 2 pi (y0 - t), 2 pi (x0 + y0 - t) at
   // the centroid; per point only small-angle Taylor rotations follow
   const double x0 = a1x + (B11 + B12) * (1.0 / 3.0), y0 = a1y + (B21 + B22) * (1.0 / 3.0);
   double sx0 = 0.0, cx0 = 1.0, sy0 = 0.0, cy0 = 1.0, sxy0 = 0.0, cxy0 = 1.0;
-  if (tay) {
+  if (tay || uni) {
     sincospi(2.0 * (x0 - t), &sx0, &cx0);
     sincospi(2.0 * (y0 - t), &sy0, &cy0);
     sincospi(2.0 * (x0 + y0 - t), &sxy0, &cxy0);
@@ -615,7 +621,13 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
     const double r1 = s_tab[TB::QR1 + q], r2 = s_tab[TB::QR2 + q];
     const double x = fma(B11, r1, fma(B12, r2, x0)), y = fma(B21, r1, fma(B22, r2, y0));
     double S, Fx, Fy;
-    if (tay) {
+    if (uni) {
+      const double* o = su_e + 6 * q;
+      const double sz = o[0], cz = o[1], sw = o[2], cw = o[3], szw = o[4], czw = o[5];
+      forcing_mms<(V & V_FRIC) != 0>(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
+                  fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
+                  fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
+    } else if (!(V & V_UNI) && tay) {
       double sz, cz, sw, cw;
       if ((V & V_TAY7) || P.taylor == 2) {
         sincos_small7(fma(t11, r1, t12 * r2), sz, cz);
@@ -628,7 +640,7 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
       forcing_mms<(V & V_FRIC) != 0>(P, x, y, fma(sxy0, czw, cxy0 * szw), fma(cxy0, czw, -sxy0 * szw),
                   fma(sx0, cz, cx0 * sz), fma(cx0, cz, -sx0 * sz), fma(sy0, cw, cy0 * sw),
                   fma(cy0, cw, -sy0 * sw), S, Fx, Fy);
-    } else if constexpr (!(V & V_TAY7)) {
+    } else if constexpr (!(V & (V_TAY7 | V_UNI))) {
       forcing(P, x, y, t, st, ct, S, Fx, Fy);
     }
     sink(s_tab + TB::P + q * K, S * sd, Fx * sd, Fy * sd);
@@ -642,7 +654,8 @@ template <int k>
 size_t stage_smem_bytes(int hc) {
   constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
   constexpr int NF = FS<k>::value;
-  return sizeof(double) * (3 * NF * NT * Blk<k>::value + NF * NT * hc + 3 * K * NT) +
+  constexpr int NU = k <= 2 ? uni_size(Ord<k>::NQ) : 0;  // MMS phase-offset table
+  return sizeof(double) * (3 * NF * NT * Blk<k>::value + NF * NT * hc + 3 * K * NT + NU) +
          sizeof(int) * (hc + 8);
 }
 
@@ -660,7 +673,9 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double* s_tr = smem;  // trace exchange [3 edges][NF fields][NT][BS]
   double* s_ht = s_tr + 3 * NF * NT * BS;  // out-of-block neighbour traces [NF][NT][HC]
   double* s_L = s_ht + NF * NT * HC;       // Lambda [3][K][NT] (neighbour edge varies by lane)
-  int* s_req = reinterpret_cast<int*>(s_L + 3 * K * NT);  // [HC] neighbour codes, then count
+  constexpr int NU = k <= 2 ? uni_size(NQ) : 0;
+  double* s_U = s_L + 3 * K * NT;          // MMS phase-offset table (Tab::uni), k <= 2
+  int* s_req = reinterpret_cast<int*>(s_U + NU);  // [HC] neighbour codes, then count
   const double* s_tab = TB::ptr();  // per-order constants (constant memory, uniform reads)
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
@@ -700,6 +715,15 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const int WC = HC / NW;
   int* s_cnt = s_req + HC;  // [NW] requests per warp
   int hs[3] = {-1, -1, -1};
+  // MMS phase-offset table to shared memory (made visible by the barrier
+  // after phase A2, before the source terms)
+  const double* su = nullptr;
+  if constexpr (k <= 2 && !(V & V_TAY7)) {
+    if ((V & V_UNI) || ((V & V_FC) && T.uni != nullptr)) {
+      for (int i = slot; i < NU; i += BS) s_U[i] = T.uni[i];
+      su = s_U;
+    }
+  }
   if (edges) {
     for (int i = slot; i < 3 * K * NT; i += BS) s_L[i] = s_tab[TB::L + i];
     const int lane = slot & 31, w = slot >> 5;
@@ -865,7 +889,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       }
     }
     if ((V & V_FC) && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
-      forcing_quad<k, V>(P, T, e, t, B11, B12, B21, B22, sd,
+      forcing_quad<k, V>(P, T, e, t, B11, B12, B21, B22, sd, su,
                       [&](const double* Pq, double S, double Fx, double Fy) {
 #pragma unroll
                         for (int p = 0; p < K; ++p) {
@@ -1731,7 +1755,22 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
              ((QF_LEAN_INST >> k) & 1)) {
     v = (P.forcing ? V_FC : 0) | (x->d.n_bnd > 0 ? V_DIR : 0) | (P.hb_linear ? 0 : V_HBC) |
         (x->walls ? V_WALL : 0) | (ovf ? V_OVF : 0) | V_STG;
-    if (P.forcing && P.kind == SCN_MMS && P.taylor == 2) v |= V_TAY7;
+    if (P.forcing && P.kind == SCN_MMS) {
+      if (k <= 2 && x->tab.uni) v |= V_UNI;
+      else if (P.taylor == 2) v |= V_TAY7;
+    }
+  }
+  if constexpr (k <= 2) {  // BASELINE MMS on a uniform split-square mesh (C1, C2)
+    if (v == (V_STG | V_FC | V_DIR | V_UNI)) {
+      stage_inst<k, V_STG | V_FC | V_DIR | V_UNI>(x, a, s, grid, smem);
+      g_launches++;  // (k <= 2: no velocity launch follows)
+      return;
+    }
+    if (v == (V_STG | V_FC | V_DIR | V_UNI | V_OVF)) {
+      stage_inst<k, V_STG | V_FC | V_DIR | V_UNI | V_OVF>(x, a, s, grid, smem);
+      g_launches++;  // (k <= 2: no velocity launch follows)
+      return;
+    }
   }
   switch (v) {
     case V_STG | V_FC | V_DIR | V_TAY7:  // BASELINE MMS at small element size (C2)
@@ -1818,7 +1857,7 @@ static void launch_l2(qf_ctx* x, const double* c, double t, int e0, int n, int n
 
 extern "C" {
 
-int qf_abi_version(void) { return 1; }
+int qf_abi_version(void) { return 2; }
 const char* qf_last_error(void) { return g_last_error.c_str(); }
 uint64_t qf_launch_count(void) { return g_launches.load(); }
 
@@ -1839,7 +1878,8 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
       x->n_sm = nsm;
   }
   x->NT = d->order + 1;
-  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->hbt, d->ld, d->n_bnd};
+  x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->hbt, d->ld, d->n_bnd,
+               d->order <= 2 ? d->uni : nullptr};
   x->phys.g = d->g;
   x->phys.fc = d->f_c;
   x->phys.tau = d->tau_bf;

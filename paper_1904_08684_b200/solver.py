@@ -26,7 +26,7 @@ import numpy as np
 from . import _cabi
 from .layout import BND_DIRICHLET, build_tables, pad_ld
 from .mesh import ElementGeometry, Mesh, compute_geometry, locality_order
-from .scenario import KIND_NONE, Scenario
+from .scenario import KIND_MMS, KIND_NONE, Scenario
 from .symbolic import build_basis
 from .tensors import build_ref_tensors, triangle_rule
 
@@ -336,6 +336,9 @@ class Discretization(HostSetup):
         # (|z| <= 0.06), 2 = degree 7/6 (|z| <= 0.02); truncation < 1e-18
         ang = self._max_quad_angle()
         d.taylor = 2 if ang <= 0.02 else (1 if ang <= 0.06 else 0)
+        uni = self._uniform_phase_table() if d.has_forcing else None
+        self._uni = None if uni is None else torch.from_numpy(uni).to(dev)
+        d.uni = None if uni is None else self._uni.data_ptr()
         self._desc = d
         ctx = _cabi.C.c_void_p()
         _cabi.check(lib.qf_create(_cabi.C.byref(d), _cabi.C.byref(ctx)), "qf_create")
@@ -353,6 +356,35 @@ class Discretization(HostSetup):
                                        self._stream), "qf_project")
             self._c_init = c0
             self._raise_errors("initial projection")
+
+    def _uniform_phase_table(self):
+        """MMS forcing on a mesh whose element Jacobians take at most two
+        values (the BASELINE split-square meshes at N = 2^j): sin/cos of the
+        per-point phase offsets 2 pi B (r_q - centroid) per Jacobian class,
+        so the kernel only rotates the centroid phases (qfswe.h ``uni``).
+        None when the mesh has more than two Jacobians or k > 2."""
+        if self.k > 2 or self.scn.device.kind != KIND_MMS:
+            return None
+        n = self.tables.n_elem
+        geo = self.tables.geo[:4, :n]
+        if n == 0:
+            return None
+        cls = np.unique(geo.T, axis=0)
+        if len(cls) > 2:
+            return None
+        B1 = cls[-1]
+        nq = len(self.quad_ref)
+        r = self.quad_ref - 1.0 / 3.0
+        tab = np.zeros(8 + 2 * (6 * nq + 2))
+        tab[:4] = B1
+        for c, Bc in enumerate((cls[0], B1)):
+            z = 2.0 * math.pi * (Bc[0] * r[:, 0] + Bc[1] * r[:, 1])
+            w = 2.0 * math.pi * (Bc[2] * r[:, 0] + Bc[3] * r[:, 1])
+            rows = np.stack([np.sin(z), np.cos(z), np.sin(w), np.cos(w),
+                             np.sin(z + w), np.cos(z + w)], axis=1)
+            o = 8 + c * (6 * nq + 2)
+            tab[o:o + 6 * nq] = rows.ravel()
+        return tab
 
     def _max_quad_angle(self) -> float:
         """max |2 pi (x_q - x_centroid)| over quadrature points (MMS Taylor gate)."""

@@ -299,19 +299,25 @@ def test_walls_conserve_mass_long_run(k):
 @pytest.mark.parametrize("n,level", [(96, 1), (256, 2)])
 def test_mms_taylor_forcing_matches_libm(monkeypatch, n, level):
     """The element-local Taylor sin/cos of the MMS forcing (degree 9 when
-    max|z| <= 0.06, degree 7 when <= 0.02) agrees with the sincospi path."""
+    max|z| <= 0.06, degree 7 when <= 0.02) and the tabulated offsets of a
+    two-Jacobian mesh (N = 256; N = 96 has more Jacobians: i/96 is inexact)
+    agree with the sincospi path."""
     from paper_1904_08684_b200 import mesh as M, scenario as S
     from paper_1904_08684_b200.solver import Discretization
     mesh = M.build_unit_square_mesh(n)
     scn = S.mms_scenario(dt=2e-5)
+    uni = Discretization(mesh, scn, 2)  # tabulated offsets when the mesh has <= 2 Jacobians
+    assert (uni._desc.uni is not None) == (n == 256)
+    monkeypatch.setattr(Discretization, "_uniform_phase_table", lambda self: None)
     tay = Discretization(mesh, scn, 2)
-    assert tay._desc.taylor == level
+    assert tay._desc.taylor == level and tay._desc.uni is None
     monkeypatch.setattr(Discretization, "_max_quad_angle", lambda self: 1.0)
     lib = Discretization(mesh, scn, 2)
     assert lib._desc.taylor == 0
     st = tay.project_initial()
-    a, b = tay.source_rhs(st, 0.37), lib.source_rhs(st, 0.37)
-    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+    b = lib.source_rhs(st, 0.37)
+    for a in (tay.source_rhs(st, 0.37), uni.source_rhs(st, 0.37)):
+        assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
 
 
 @pytest.mark.parametrize("k,n,steps", [(0, 8, 3), (1, 16, 20), (2, 16, 20), (3, 8, 10), (4, 6, 5)])
