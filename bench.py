@@ -44,8 +44,8 @@ CONFIGS = {
 # element (2 dfma + dmul + dadd, smsp__sass_thread_inst_executed_op_*), from
 # tools/kernel_counts.sh under ncu; summaries in profiles/r01_kernel_counts.txt
 PROFILED = {
-    "c1": {"bytes_per_elem": 288.2, "flop_per_elem": 3025.2},
-    "c2": {"bytes_per_elem": 479.9, "flop_per_elem": 5974.3},
+    "c1": {"bytes_per_elem": 284.6, "flop_per_elem": 2227.2},
+    "c2": {"bytes_per_elem": 481.4, "flop_per_elem": 5225.3},
     "c3": {"bytes_per_elem": 2328.7, "flop_per_elem": 8391.9},
     "c4": {"bytes_per_elem": 682.0, "flop_per_elem": 3289.3},
     "c5": {"bytes_per_elem": 4162.9, "flop_per_elem": 18373.4},
