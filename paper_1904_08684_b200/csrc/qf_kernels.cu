@@ -581,6 +581,15 @@ __device__ __forceinline__ void volume_terms(const Phys& P, double B11, double B
   }
 }
 
+// global -> shared 8-byte asynchronous copies (no registers held)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Manufactured forcing at the (k+2)^2 collapsed Gauss points of element e
 // (reference solver.py:719-724, scenario.py:78-93): sink(P_q, S, Fx, Fy)
 // with P_q[p] = w_q phi_p(q) and the point values already scaled by sqrt(detB).
@@ -720,7 +729,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   const double* su = nullptr;
   if constexpr (k <= 2 && !(V & V_TAY7)) {
     if ((V & V_UNI) || ((V & V_FC) && T.uni != nullptr)) {
-      for (int i = slot; i < NU; i += BS) s_U[i] = T.uni[i];
+      for (int i = slot; i < NU; i += BS) cp_async8(s_U + i, T.uni + i);  // waited before the barrier after A2
       su = s_U;
     }
   }
@@ -841,6 +850,9 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       a2_trace(hsl, fi, f, g4);
     }
   }
+  if constexpr (k <= 2 && !(V & V_TAY7)) {
+    if (su) cp_async_wait_all();  // MMS phase-offset table
+  }
   __syncthreads();
   if (!active) return;
 
@@ -959,13 +971,6 @@ struct SRow {
   __device__ __forceinline__ double operator[](int i) const { return s * p[i * 128]; }
 };
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
 // k >= 4: the volume kernel copies its element's 3K state rows into shared
 // memory with one burst of cp.async (no registers held, every load in flight
