@@ -244,9 +244,11 @@ def run_gpu(args):
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
     ns = stages_of(k)
 
-    def step():  # the library's SSP-RK step: 1 Dirichlet-data + ns stage launches + t advance
-        _cabi.check(lib.qf_step(disc._ctx, ds.c.data_ptr(), ds.u.data_ptr(), work.data_ptr(),
-                                ds.t_dev.data_ptr(), sp), "qf_step")
+    def step():  # the library's SSP-RK step: 1 Dirichlet-data + ns stage launches + t advance,
+        # replayed as one CUDA graph (qf_run, as Discretization.run does): a host stall between
+        # kernel launches cannot open a gap inside the timed step
+        _cabi.check(lib.qf_run(disc._ctx, 1, ds.c.data_ptr(), ds.u.data_ptr(), work.data_ptr(),
+                               ds.t_dev.data_ptr(), 1, sp), "qf_run")
 
     for _ in range(args.warmup):
         step()
