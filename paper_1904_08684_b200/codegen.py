@@ -167,8 +167,11 @@ def gen_order(k: int) -> str:
             w(f"    A[{m * (m + 1) // 2 + p}] = {_sum(terms)};")
     w("  }")
     # ---- LDL^T velocity solve in scalar registers (no local arrays)
+    # (qU, qV: register arrays, or strided row views read where the forward
+    # substitution first needs them)
+    w("  template <class Q>")
     w("  static __device__ __forceinline__ bool vel_solve(const double* __restrict__ H,"
-      " const double* qU, const double* qV, double sd, double* uo, double* vo) {")
+      " const Q& qU, const Q& qV, double sd, double* uo, double* vo) {")
     for m in range(K):
         for p in range(m + 1):
             terms = [(rt.G[p, i, m], f"H[{i}]") for i in range(K) if _nz(rt.G[p, i, m])]

@@ -1291,6 +1291,15 @@ __global__ void __launch_bounds__(128, QF_VMMA_MINB) vol_mma_kernel(Tab T, const
 #ifndef QF_VELOCC4
 #define QF_VELOCC4 1
 #endif
+#ifndef QF_VLAZY
+#define QF_VLAZY 4
+#endif
+// strided read-only view of one state row, read on use
+struct QRow {
+  const double* p;
+  int64_t ld;
+  __device__ __forceinline__ double operator[](int i) const { return ldv(p + i * ld); }
+};
 #ifndef QF_VELOCC3
 #define QF_VELOCC3 3  // k = 3 velocity at 168 registers: 358 -> 350 us/stage (N = 512)
 #endif
@@ -1307,15 +1316,26 @@ __global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : (k == 3 ? QF_VELOCC
   const double B11 = ldg(T.geo + e), B12 = ldg(T.geo + ld + e);
   const double B21 = ldg(T.geo + 2 * ld + e), B22 = ldg(T.geo + 3 * ld + e);
   const double sd = sqrt(det2(B11, B12, B21, B22));
-  double cc[3 * K], hb[K], uo[K], vo[K];
+  // k >= QF_VLAZY: the U, V rows are read where the forward substitution
+  // first needs them instead of being held through the factorisation
+  constexpr bool LAZY = k >= QF_VLAZY;
+  constexpr int NC = LAZY ? K : 3 * K;
+  double cc[NC], hb[K], uo[K], vo[K];
 #pragma unroll
-  for (int i = 0; i < 3 * K; ++i) cc[i] = ldg(c + i * ld + e);
+  for (int i = 0; i < NC; ++i) cc[i] = ldg(c + i * ld + e);
 #pragma unroll
   for (int i = 0; i < K; ++i) hb[i] = i < NH ? ldg(T.hb + i * ld + e) : 0.0;
   double H[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) H[i] = cc[i] + hb[i];
-  if (!O::vel_solve(H, cc + K, cc + 2 * K, sd, uo, vo)) atomicOr(err, BIT_SINGULAR);
+  bool ok;
+  if constexpr (LAZY) {
+    const QRow qu{c + K * ld + e, ld}, qv{c + 2 * K * ld + e, ld};
+    ok = O::vel_solve(H, qu, qv, sd, uo, vo);
+  } else {
+    ok = O::vel_solve(H, cc + K, cc + 2 * K, sd, uo, vo);
+  }
+  if (!ok) atomicOr(err, BIT_SINGULAR);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     u[i * ld + e] = uo[i];
