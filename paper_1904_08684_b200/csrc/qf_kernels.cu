@@ -988,8 +988,11 @@ struct SRow {
 #ifndef QF_VOCC4
 #define QF_VOCC4 3
 #endif
+#ifndef QF_VOCC4G0  // k = 4 output group 0 (the larger one): 2 blocks/SM, no spills
+#define QF_VOCC4G0 2    // (858 -> 848 us per k = 4 stage at N = 512 against 3 blocks/SM)
+#endif
 template <int k, int GRP = 0, bool HBC = true>  // HBC: hb_mode "const" code compiled
-__global__ void __launch_bounds__(128, k == 4 ? QF_VOCC4 : QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
+__global__ void __launch_bounds__(128, k == 4 ? (GRP == 0 ? QF_VOCC4G0 : QF_VOCC4) : QF_VOCC) volume_kernel(Tab T, Phys P, const double* __restrict__ c,
                                                      const double* __restrict__ u, int e0, int n,
                                                      double* __restrict__ vol) {
   using O = Ord<k>;
