@@ -48,7 +48,7 @@ PROFILED = {
     "c2": {"bytes_per_elem": 481.4, "flop_per_elem": 5225.3},
     "c3": {"bytes_per_elem": 2328.7, "flop_per_elem": 8391.9},
     "c4": {"bytes_per_elem": 682.0, "flop_per_elem": 3289.3},
-    "c5": {"bytes_per_elem": 4169.0, "flop_per_elem": 18385.4},
+    "c5": {"bytes_per_elem": 4125.5, "flop_per_elem": 18373.4},
 }
 # FP64 FMA-pipe peak of this B200, measured by tools/micro/fp64_pipes.cu
 # (DFMA 35.3 TF/s, DMMA 37.1 TF/s, one shared pipe; profiles/r01_fp64_pipes.txt)
