@@ -11,9 +11,11 @@ coefficient of (xi, U, V) advanced through one stage (3*K*E per stage).
 Timing: CUDA events on the launching stream around each step, max over
 ranks; the 131k-element C2 state (19 MB) fits in L2, so L2 is flushed
 (a 256 MB write) between timed steps and the flush is outside the events.
-Per-stage events also time the dominant kernel (stage_kernel) for the
-roofline.  ``e2e`` is measured through ``Discretization.step`` with host
-(numpy) states: H2D of c, step, D2H of (c, u) every step.
+Event-record nodes inside the replayed step graph time every RK stage (the
+dominant kernel) for the roofline.  ``e2e`` is a dependent host-buffer
+chain through the C ABI (each step uploads what the previous one
+downloaded).  ``per_config`` repeats the measurement for the other BASELINE
+orders (C1, C3, C4, C5) with the same method.
 """
 
 from __future__ import annotations
@@ -211,9 +213,6 @@ def run_reference(args):
 def run_gpu(args):
     import torch
 
-    from paper_1904_08684_b200 import _cabi
-    from paper_1904_08684_b200.solver import Discretization
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -229,8 +228,52 @@ def run_gpu(args):
         return QD.bench_distributed(args, CONFIGS, METRIC,
                                     hooks={"clocks": lambda: Clocks(local), "peaks": peaks,
                                            "alg_bytes": alg_bytes_per_elem})
+    res = measure(args.config, args.steps, args.warmup, local, n=args.n, e2e=not args.no_e2e)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "DoF-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+    }
+    line.update({k_: v for k_, v in res.items() if k_ not in ("value", "ms_per_step")})
+    if rank == 0 and not args.no_cpu:
+        cb = cpu_baseline(args.config)
+        line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+    if args.extra and args.n is None:
+        # every other BASELINE order on the same box, same timing method
+        # (graph-replayed steps, per-stage events inside the graph): the
+        # metric is quoted for p = 1..4
+        per = {}
+        for cfg in sorted(CONFIGS):
+            if cfg == args.config:
+                continue
+            try:
+                r = measure(cfg, min(args.steps, 20), 3, local, e2e=False)
+                per[cfg] = {k_: r[k_] for k_ in ("value", "ms_per_step", "roofline", "clocks",
+                                                 "config", "checks", "gpu_launches", "setup_s")}
+            except Exception as err:  # keep the headline line even if one config fails
+                per[cfg] = {"error": f"{type(err).__name__}: {err}"}
+            torch.cuda.empty_cache()
+        line["per_config"] = per
+    print(json.dumps(line), flush=True)
+
+
+def measure(cfg, steps, warmup, local, n=None, e2e=False):
+    """One configuration on this GPU: ``steps`` timed SSP-RK steps, each one
+    replay of the library's captured step graph (qf_run, as
+    Discretization.run does) bracketed by CUDA events on the launching
+    stream, L2 flushed (256 MB write) between steps outside the events.
+    Event-record nodes inside the graph (qf_stage_events) time every RK stage
+    of the same replays, which gives the dominant kernel's launch time for
+    the roofline."""
+    import torch
+
+    from paper_1904_08684_b200 import _cabi
+    from paper_1904_08684_b200.solver import Discretization
+
     lib = _cabi.load()
-    k, n, mesh, scn = build_problem(args.config, args.n)
+    t_setup = time.perf_counter()
+    k, n_, mesh, scn = build_problem(cfg, n)
     disc = Discretization(mesh, scn, k)
     st0 = disc.project_initial()
     K, E, ld = disc.K, mesh.n_triangles, disc.ld
@@ -238,93 +281,78 @@ def run_gpu(args):
     if st0._dev is not None:  # device-set-up state: step a copy, keep st0 initial
         ds = ds.clone()
     ds.t_dev[1] = disc.dt
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
     work = disc._work_buf()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
     ns = stages_of(k)
 
-    def step():  # the library's SSP-RK step: 1 Dirichlet-data + ns stage launches + t advance,
-        # replayed as one CUDA graph (qf_run, as Discretization.run does): a host stall between
-        # kernel launches cannot open a gap inside the timed step
+    def step():  # 1 Dirichlet-data + ns stage launches + t advance, one graph replay
         _cabi.check(lib.qf_run(disc._ctx, 1, ds.c.data_ptr(), ds.u.data_ptr(), work.data_ptr(),
                                ds.t_dev.data_ptr(), 1, sp), "qf_run")
 
-    for _ in range(args.warmup):
+    def timed_steps(nsteps, sev=None, clocks=None):
+        step_ms, stage_ms = [], []
+        for it in range(nsteps):
+            flush.fill_(float(it))  # outside the timed events
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            step()
+            ev1.record(stream)
+            if clocks:
+                clocks.sample()
+            torch.cuda.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            if sev:
+                stage_ms.append([sev[2 * i].elapsed_time(sev[2 * i + 1]) for i in range(ns)])
+        return step_ms, stage_ms
+
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    # ---- pass A (the reported value): whole steps, L2 flushed between steps
+    # pass A (the reported value): plain graph replays
     clocks = Clocks(local)
     n0 = lib.qf_launch_count()
-    step_ms = []
-    for it in range(args.steps):
-        flush.fill_(float(it))  # outside the timed events
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        step()
-        ev1.record(stream)
-        clocks.sample()
-        torch.cuda.synchronize()
-        step_ms.append(ev0.elapsed_time(ev1))
+    step_ms, _ = timed_steps(steps, clocks=clocks)
     launches = lib.qf_launch_count() - n0
+    # pass B (roofline): the same step graph re-captured with event-record
+    # nodes around every RK stage (qf_stage_events); kernel share = stage
+    # time / step time of the same replays (the event nodes add a few us per
+    # step, so pass B's step time is not the reported one)
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * ns)]
+    for e_ in sev:
+        e_.record(stream)  # creates the CUDA events
+    handles = (_cabi.C.c_void_p * (2 * ns))(*[e_.cuda_event for e_ in sev])
+    _cabi.check(lib.qf_stage_events(disc._ctx, handles, 2 * ns), "qf_stage_events")
+    step()
+    torch.cuda.synchronize()
+    stepB_ms, stage_ms = timed_steps(min(steps, 50), sev=sev)
+    _cabi.check(lib.qf_stage_events(disc._ctx, None, 0), "qf_stage_events")
     clk = clocks.stop()
     disc._raise_errors("bench")
     checks = state_checks(disc, st0, ds, E)
-    # ---- pass B (roofline): the same stages with an event pair around each
-    # stage_kernel launch (qf_stage), L2 flushed between steps as in pass A
-    S5, S3 = 5 * K * ld, 3 * K * ld
-    bufs = {0: (ds.c, ds.u), 1: (work[:S3], work[S3:S5]), 2: (work[S5:S5 + S3], work[S5 + S3:])}
-    plan = [(0, 1), (1, 2), (2, 0)] if k >= 2 else ([(0, 1), (1, 0)] if k == 1 else [(0, 1)])
-    has_bnd = disc.tables.bnd_elem.size > 0
-    stage_ms = []
-    tnow = float(ds.t_dev[0].item())
-    for it in range(min(args.steps, 50)):
-        flush.fill_(float(it))
-        evs = []
-        for (src, dst), (a, b, toff) in zip(plan, rk_coeffs(k)):
-            ts = tnow + toff * disc.dt
-            if has_bnd:
-                _cabi.check(lib.qf_ghost(disc._ctx, ts, sp), "qf_ghost")
-            (ci, ui), (co, uo) = bufs[src], bufs[dst]
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _cabi.check(lib.qf_stage(disc._ctx, ci.data_ptr(), ui.data_ptr(), ds.c.data_ptr(),
-                                     co.data_ptr(), uo.data_ptr(), a, b, ts, disc.dt, None, 0.0,
-                                     0, -1, sp), "qf_stage")
-            e1.record(stream)
-            evs.append((e0, e1))
-        if k == 0:
-            ds.c.copy_(bufs[1][0])
-            ds.u.copy_(bufs[1][1])
-        tnow += disc.dt
-        torch.cuda.synchronize()
-        stage_ms.append([a.elapsed_time(b) for a, b in evs])
     total_ms = float(np.sum(step_ms))
-    dof = 3 * K * E * ns * args.steps
-    value = dof / (total_ms * 1e-3)
+    value = 3 * K * E * ns * steps / (total_ms * 1e-3)
     peak, peak_src = peaks()
     st = np.array(stage_ms)
     rvec = [0] + [1] * (ns - 1)
     bytes_step = sum(E * alg_bytes_per_elem(K, r) for r in rvec)
     kern_ms_step = float(st.sum(axis=1).mean())
     achieved = bytes_step / (kern_ms_step * 1e-3) / 1e9
-    prof = PROFILED.get(args.config) if args.n is None else None
+    prof = PROFILED.get(cfg) if n is None else None
     fp64 = None
     if prof:
         tf = prof["flop_per_elem"] * E * ns / (kern_ms_step * 1e-3) / 1e12
         fp64 = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / FP64_PEAK_TFLOPS, "flop_per_elem_stage": prof["flop_per_elem"],
                 "peak_source": "measured DFMA throughput (tools/micro/fp64_pipes.cu)"}
-    e2e = None if args.no_e2e else measure_e2e(disc, st0, max(3, min(args.steps, 100)))
-    cb = cpu_baseline(args.config) if rank == 0 and not args.no_cpu else None
-    line = {
-        "metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+    out = {
+        "value": value, "ms_per_step": total_ms / steps,
         "step_ms": {"min": float(np.min(step_ms)), "median": float(np.median(step_ms)),
                     "max": float(np.max(step_ms))},
-        "config": {"workload": CONFIGS[args.config][5], "order": k, "n": n, "elements": E,
+        "config": {"workload": CONFIGS[cfg][5], "order": k, "n": n_, "elements": E,
                    "K": K, "stages_per_step": ns, "dt": disc.dt,
                    "dof_per_stage": 3 * K * E, "l2": "flushed (256 MB write) between timed steps",
                    "parallelism": "single GPU"},
@@ -335,21 +363,22 @@ def run_gpu(args):
                                      "stages of an L2-flushed step), algorithmic: "
                                      f"{bytes_step / ns:.4g}",
                      "peak_source": peak_src,
-                     "kernel": "stage_kernel" if k <= 2 else
-                               "stage (volume_kernel + stage_kernel + velocity_kernel)",
+                     "kernel": "stage_kernel (one RK stage; timed by event-record nodes "
+                               "inside the replayed step graph)",
                      "kernel_ms_per_step": kern_ms_step, "alg_bytes_per_step": bytes_step,
-                     "kernel_share_of_step": kern_ms_step / (total_ms / args.steps),
+                     "kernel_share_of_step": kern_ms_step / float(np.mean(stepB_ms)),
                      "fp64": fp64},
         "hbm_roofline_dof_per_s": 3 * K * E * ns / (bytes_step / (peak * 1e9)),
-        "e2e": e2e,
         "gpu_launches": int(launches),
         "checks": checks,
         "clocks": clk,
+        "setup_s": setup_s,
     }
-    line["roofline_frac_dof"] = value / line["hbm_roofline_dof_per_s"]
-    if cb is not None:
-        line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
-    print(json.dumps(line), flush=True)
+    out["roofline_frac_dof"] = value / out["hbm_roofline_dof_per_s"]
+    if e2e:
+        out["e2e"] = measure_e2e(disc, st0, max(3, min(steps, 50)))
+    del disc, ds, work, flush
+    return out
 
 
 def state_checks(disc, st0, ds, E):
@@ -370,18 +399,18 @@ def state_checks(disc, st0, ds, E):
 
 
 def measure_e2e(disc, st0, steps):
-    """End to end through the C ABI with HOST buffers (pinned numpy arrays in the
-    reference's (E, F, K) State layout).  Every step: H2D of the input state c,
-    qf_pack, qf_velocity, qf_step, qf_unpack, D2H of the new state c.
+    """End to end through the C ABI with HOST buffers (pinned numpy arrays in
+    the reference's (E, 3, K) State layout), as a DEPENDENT time-stepping
+    chain: step i uploads the state that step i-1 downloaded.  Every step,
+    in stream order: H2D of c, qf_pack, qf_velocity, qf_step (one SSP-RK step),
+    qf_unpack, D2H of the new c into the buffer the next step uploads; CUDA
+    events around all steps.  Nothing overlaps across steps (no step can start
+    before its input has come back to the host).
 
-    ``value``: the steps are pipelined over three streams (H2D of the next
-    steps and D2H of the previous ones overlap the kernels of step i;
-    double-buffered device staging), CUDA events around all K steps.  Bound:
-    concurrent H2D + D2H of the 8*3*K*E-byte state per step (C2: 0.405 ms per
-    step on the bench box, tools/pcie_bw.py).  ``serial``: the same sequence
-    on one stream, each step also reading back u.  Also reports
-    Discretization.step (the Python API, numpy in/out) wall clock as
-    ``public_api``."""
+    Also reported: ``public_api`` = ``Discretization.step`` on numpy States
+    (the call a reference user makes; persistent pinned staging, c and u
+    read back every step), and ``run_api`` = ``Discretization.run`` (one
+    upload, graph-replayed steps, one download), both wall clock."""
     import torch
 
     from paper_1904_08684_b200 import _cabi
@@ -389,14 +418,10 @@ def measure_e2e(disc, st0, steps):
 
     lib = disc._lib
     E, K, ld = disc.mesh.n_triangles, disc.K, disc.ld
-    h_c = torch.empty((E, 3, K), dtype=torch.float64).pin_memory()
-    h_out_c = torch.empty((E, 3, K), dtype=torch.float64).pin_memory()
-    h_out_u = torch.empty((E, 2, K), dtype=torch.float64).pin_memory()
-    h_c.numpy()[:] = st0.c
-    NB = 2  # staging depth (H2D-bound: 2 slots keep the H2D stream busy)
-    d_in = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(NB)]
-    d_out = [torch.empty((E, 3, K), dtype=torch.float64, device="cuda") for _ in range(NB)]
-    d_u = torch.empty((E, 2, K), dtype=torch.float64, device="cuda")
+    h = [torch.empty((E, 3, K), dtype=torch.float64).pin_memory() for _ in range(2)]
+    h[0].numpy()[:] = st0.c
+    d_in = torch.empty((E, 3, K), dtype=torch.float64, device="cuda")
+    d_out = torch.empty((E, 3, K), dtype=torch.float64, device="cuda")
     c, u = disc._empty_state()
     c.zero_()
     u.zero_()
@@ -404,88 +429,62 @@ def measure_e2e(disc, st0, steps):
     work = disc._work_buf()
     pp = disc._perm_ptr(E)
     s_cmp = torch.cuda.current_stream()
-    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(NB)]    # H2D into slot done
-    ev_used = [torch.cuda.Event() for _ in range(NB)]  # pack consumed slot
-    ev_res = [torch.cuda.Event() for _ in range(NB)]   # result unpacked into slot
-    ev_out = [torch.cuda.Event() for _ in range(NB)]   # D2H of slot done
+    sp = s_cmp.cuda_stream
 
-    def kernels(din, dout, sp, with_u=False):
-        _cabi.check(lib.qf_pack(din.data_ptr(), c.data_ptr(), E, 3, K, ld, pp, sp), "pack")
-        _cabi.check(lib.qf_velocity(disc._ctx, c.data_ptr(), u.data_ptr(), 0, -1, sp), "vel")
-        _cabi.check(lib.qf_step(disc._ctx, c.data_ptr(), u.data_ptr(), work.data_ptr(),
-                                tdev.data_ptr(), sp), "step")
-        _cabi.check(lib.qf_unpack(c.data_ptr(), dout.data_ptr(), E, 3, K, ld, pp, sp), "unpack")
-        if with_u:
-            _cabi.check(lib.qf_unpack(u.data_ptr(), d_u.data_ptr(), E, 2, K, ld, pp, sp), "unpack")
-
-    def pipelined(n):
+    def chain(n):
         for i in range(n):
-            b = i % NB
-            with torch.cuda.stream(s_h2d):
-                s_h2d.wait_event(ev_used[b])
-                d_in[b].copy_(h_c, non_blocking=True)
-                ev_in[b].record(s_h2d)
-            s_cmp.wait_event(ev_in[b])
-            s_cmp.wait_event(ev_out[b])
-            kernels(d_in[b], d_out[b], s_cmp.cuda_stream)
-            ev_used[b].record(s_cmp)
-            ev_res[b].record(s_cmp)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_res[b])
-                h_out_c.copy_(d_out[b], non_blocking=True)
-                ev_out[b].record(s_d2h)
-        s_cmp.wait_stream(s_h2d)
-        s_cmp.wait_stream(s_d2h)
+            src, dst = h[i % 2], h[(i + 1) % 2]
+            d_in.copy_(src, non_blocking=True)
+            _cabi.check(lib.qf_pack(d_in.data_ptr(), c.data_ptr(), E, 3, K, ld, pp, sp), "pack")
+            _cabi.check(lib.qf_velocity(disc._ctx, c.data_ptr(), u.data_ptr(), 0, -1, sp), "vel")
+            _cabi.check(lib.qf_step(disc._ctx, c.data_ptr(), u.data_ptr(), work.data_ptr(),
+                                    tdev.data_ptr(), sp), "step")
+            _cabi.check(lib.qf_unpack(c.data_ptr(), d_out.data_ptr(), E, 3, K, ld, pp, sp),
+                        "unpack")
+            dst.copy_(d_out, non_blocking=True)
 
-    def serial():
-        d_in[0].copy_(h_c, non_blocking=True)
-        kernels(d_in[0], d_out[0], s_cmp.cuda_stream, with_u=True)
-        h_out_c.copy_(d_out[0], non_blocking=True)
-        h_out_u.copy_(d_u, non_blocking=True)
-
-    def timed(fn, *a):
-        fn(*a)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn(*a)
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
-
-    ms_pipe = timed(pipelined, steps)  # (pipeline fill / drain amortised over the steps)
-    n_pipe, steps = steps, min(steps, 20)
-    ms_ser = sum(timed(serial) for _ in range(steps))
+    chain(2)
+    torch.cuda.synchronize()
+    h[0].numpy()[:] = st0.c
+    tdev[0] = st0.t
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    chain(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    disc._raise_errors("e2e")
     ns = stages_of(disc.k)
     dof = 3 * K * E * ns
     # the Python API (numpy State in, numpy State out), wall clock
+    api_steps = min(steps, 20)
     st = disc.step(State(st0.c.copy(), st0.u.copy(), st0.t))
     _ = st.c
     t0 = time.perf_counter()
-    for _ in range(steps):
+    for _ in range(api_steps):
         st = disc.step(State(st.c, st.u, st.t))
         _ = st.c
     api = time.perf_counter() - t0
-    # the whole-run public API: Discretization.run(numpy State, t_end) -- one
-    # upload of c, n_pipe graph-replayed steps, the error word read once, one
-    # download of the final State (c and u), wall clock
-    t_end = st0.t + n_pipe * disc.dt
+    # Discretization.run(numpy State, t_end): one upload of c, graph-replayed
+    # steps, the error word read once, one download of c and u, wall clock
+    t_end = st0.t + steps * disc.dt
     _ = disc.run(State(st0.c.copy(), st0.u.copy(), st0.t), t_end=t_end).c
     t0 = time.perf_counter()
     _ = disc.run(State(st0.c.copy(), st0.u.copy(), st0.t), t_end=t_end).c
     run_s = time.perf_counter() - t0
-    return {"value": dof * n_pipe / (ms_pipe * 1e-3), "unit": "DoF-updates/s",
+    return {"value": dof * steps / (ms * 1e-3), "unit": "DoF-updates/s",
             "h2d_bytes_per_step": 8 * 3 * K * E, "d2h_bytes_per_step": 8 * 3 * K * E,
-            "timing": "C ABI with pinned host State buffers, every step: H2D c, qf_pack, "
-                      "qf_velocity, qf_step, qf_unpack, D2H c; steps pipelined over H2D / "
-                      "compute / D2H streams; CUDA events around all steps",
-            "serial": {"value": dof * steps / (ms_ser * 1e-3), "unit": "DoF-updates/s",
-                       "d2h_bytes_per_step": 8 * 5 * K * E,
-                       "timing": "same sequence on one stream, D2H of c and u, per-step events"},
-            "public_api": {"value": dof * steps / api, "unit": "DoF-updates/s",
-                           "timing": "Discretization.step with numpy States, wall clock"},
-            "run_api": {"value": dof * n_pipe / run_s, "unit": "DoF-updates/s", "steps": n_pipe,
+            "steps": steps,
+            "timing": "C ABI, dependent chain: each step uploads (pinned H2D) the state the "
+                      "previous step downloaded; H2D c, qf_pack, qf_velocity, qf_step, "
+                      "qf_unpack, D2H c on one stream; CUDA events around all steps",
+            "public_api": {"value": dof * api_steps / api, "unit": "DoF-updates/s",
+                           "ms_per_step": 1e3 * api / api_steps,
+                           "h2d_bytes_per_step": 8 * 3 * K * E,
+                           "d2h_bytes_per_step": 8 * 5 * K * E,
+                           "timing": "Discretization.step with numpy States (c and u read "
+                                     "back every step), wall clock"},
+            "run_api": {"value": dof * steps / run_s, "unit": "DoF-updates/s", "steps": steps,
                         "h2d_bytes_per_run": 8 * 3 * K * E, "d2h_bytes_per_run": 8 * 5 * K * E,
                         "timing": "Discretization.run(numpy State, t_end) over the steps: one "
                                   "upload of c, graph-replayed steps, error word read once, "
@@ -508,6 +507,8 @@ def main():
                     help="N > 1 halo exchange: the fused push (stage kernels store into the "
                          "peers' halo slots over CUDA IPC / NVLink; all ranks fall back to NCCL "
                          "together if a peer mapping fails), or NCCL send/recv")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the per_config lines (the other BASELINE orders)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU runner even at world size 1 (smoke test)")
     args = ap.parse_args()

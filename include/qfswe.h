@@ -18,9 +18,11 @@
  *  - Every call returns a status: QF_OK, or QF_E_* below.  Asynchronous
  *    numerical faults (dry state, singular projection, non-finite values)
  *    are latched in a device error word read with qf_error().
- *  - One context per (process, device); calls on one context must be
- *    serialised by the caller (same as the reference's single-threaded
- *    Discretization).
+ *  - One context per (process, device): qf_create binds the caller's
+ *    current device; every entry point taking a context makes that device
+ *    current for the call and restores the caller's afterwards.  Calls on
+ *    one context must be serialised by the caller (same as the reference's
+ *    single-threaded Discretization).
  */
 #ifndef QFSWE_H
 #define QFSWE_H
@@ -127,6 +129,13 @@ int qf_rhs(qf_ctx* ctx, const double* c, const double* u, double t, int32_t term
 int qf_rhs_mass(qf_ctx* ctx, const double* c, const double* u, double t, int32_t terms,
                 double* rhs, double* lam, double* mflux, void* stream);
 
+/* qf_rhs_mass with a caller-supplied lambda (reference edge_rhs(state, t,
+ * lam), solver.py:690-704): lam_in (device [3][ld], may be NULL) is the
+ * Lax-Friedrichs speed each element uses on its local edges instead of the
+ * recomputed one (both sides of an edge must carry the same value). */
+int qf_rhs_ex(qf_ctx* ctx, const double* c, const double* u, double t, int32_t terms,
+              double* rhs, double* lam, double* mflux, const double* lam_in, void* stream);
+
 /* One SSP-RK stage (solver.py:750-764) for elements [e0, e0+n):
  *   c_out = a*c0 + b*(c_in + dt*rhs(c_in, u_in, t)),  u_out = velocity(c_out).
  * t_dev (optional device [2] = {t_step, dt}) overrides t: t = t_dev[0] + toff*t_dev[1]. */
@@ -193,6 +202,12 @@ int qf_scatter(const double* src, const int32_t* idx, int32_t n_idx, int32_t row
  * over partitions). */
 int qf_l2_error(qf_ctx* ctx, const double* c, double t, int32_t e0, int32_t n, double* sq,
                 void* stream);
+
+/* Timing hooks (bench.py): events[2i], events[2i+1] (cudaEvent_t, timing
+ * enabled) are recorded around RK stage i of every qf_step / qf_run step,
+ * inside the captured run graph as event-record nodes, so per-stage kernel
+ * times come from the same graph replay as the step time.  n = 0 clears. */
+int qf_stage_events(qf_ctx* ctx, void* const* events, int32_t n);
 
 /* Read (and optionally clear) the error word; synchronises `stream`. */
 int qf_error(qf_ctx* ctx, uint32_t* bits, int32_t clear, void* stream);

@@ -87,6 +87,7 @@ struct StageArgs {
   const int* push;                // optional fused halo push [3][ld] (see push_rows)
   double* mflux;                  // stage_kernel<k, true>: [3][ld] xi mode-0 rhs of each edge
   const qf_peer* peers;           // device table of the peers' destination buffers
+  const double* lam_in;           // optional caller-supplied lambda [3][ld] (edge_rhs(state, t, lam))
 };
 
 // Fused halo exchange ("a trace-producer kernel stores directly
@@ -177,19 +178,12 @@ struct Blk {
 #ifndef QF_HCAP
 #define QF_HCAP 128
 #endif
-// timing experiments only (wrong numerics): in-block traces for every neighbour
-#ifndef QF_FAKE_HALO
-#define QF_FAKE_HALO 0
-#endif
 // orders whose stage kernel keeps the element's own data in registers
 #ifndef QF_PRE_MAXK
 #define QF_PRE_MAXK 2
 #endif
 #ifndef QF_NOFALLBACK
 #define QF_NOFALLBACK 0
-#endif
-#ifndef QF_FAKE_HBT
-#define QF_FAKE_HBT 0
 #endif
 // Stage-kernel instance variants (compile-time code paths; a path that cannot
 // occur on a problem is compiled out: smaller register / spill footprint)
@@ -261,13 +255,13 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     if constexpr (!HS) {
 #pragma unroll
       for (int a = 0; a < NT; ++a) {
-        const double v = QF_FAKE_HBT ? own[5][a] : ldg(T.hbt + (jn * NT + a) * ld + nb);
+        const double v = ldg(T.hbt + (jn * NT + a) * ld + nb);
         oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
       }
     }
     if (!hbl) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
-    if (QF_FAKE_HALO || (nb >= blo && nb < bhi)) {  // neighbour traced by its own thread in phase A
-      const int ns = QF_FAKE_HALO ? ((nb - blo) & (BS - 1)) : nb - blo;
+    if (nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
+      const int ns = nb - blo;
 #pragma unroll
       for (int f = 0; f < NF; ++f)
 #pragma unroll
@@ -401,7 +395,10 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
     hmin = sH[s] < hmin ? sH[s] : hmin;
   }
   if (!(hmin > 0.0)) atomicOr(A.err, BIT_DRY);
-  if (!(V & V_STG) && A.lam) A.lam[j * ld + e] = lam;
+  if constexpr (!(V & V_STG)) {
+    if (A.lam_in) lam = A.lam_in[j * ld + e];  // reference edge_rhs(state, t, lam), solver.py:690-704
+    if (A.lam) A.lam[j * ld + e] = lam;
+  }
 
   // Lax-Friedrichs flux in trace space (reference solver.py:610-613)
   double wO[NT], wN[NT], pO[NT], pN[NT], aO[NT], aN[NT], bO[NT], bN[NT];
@@ -914,11 +911,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     }
   }
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
-#ifndef QF_FAKE_NEDGE
-#define QF_FAKE_NEDGE 3
-#endif
     QF_UNROLL(QF_EUNROLL)
-    for (int j = 0; j < QF_FAKE_NEDGE; ++j)  // (timing experiments only: < 3 is wrong numerics)
+    for (int j = 0; j < 3; ++j)
       edge_term<k, Blk<k>::value, V>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
   }
@@ -1683,6 +1677,25 @@ struct qf_ctx {
   bool walls = true;         // any reflective-wall boundary code in nbr (measured in qf_create)
   bool fits = false;         // busiest warp's requests fit hcap (whole-mesh launches never overflow)
   int l2cap = 0;
+  int device = 0;            // CUDA device of the context (set around every entry point)
+  // optional timing events recorded around each stage of step_impl (also
+  // inside the captured run graph, as external event-record nodes)
+  cudaEvent_t stage_ev[8] = {};
+  int n_stage_ev = 0;
+};
+
+// makes the context's device current for the duration of an entry point
+// (restores the caller's device on exit)
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const qf_ctx* x) {
+    int cur = 0;
+    if (x && cudaGetDevice(&cur) == cudaSuccess && cur != x->device && cudaSetDevice(x->device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 static thread_local std::string g_last_error;
@@ -1709,13 +1722,16 @@ static int cuda_check(const char* what) {
   }
 
 // one stage-kernel instance: the dynamic shared-memory opt-in once per instance
+// (function attributes are per device: one opt-in bit per device ordinal;
+// a failed opt-in is not recorded, so the launch below reports the error)
 template <int k, int V>
 static void stage_inst(qf_ctx* x, const StageArgs& a, cudaStream_t s, int grid, size_t smem) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stage_kernel<k, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes<k>(QF_HCAP));
-    attr = true;
+  static std::atomic<uint64_t> attr{0};
+  const uint64_t bit = 1ull << (x->device & 63);
+  if (!(attr.load() & bit)) {
+    if (cudaFuncSetAttribute(stage_kernel<k, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)stage_smem_bytes<k>(QF_HCAP)) == cudaSuccess)
+      attr.fetch_or(bit);
   }
   stage_kernel<k, V><<<grid, Blk<k>::value, smem, s>>>(x->tab, x->phys, a);
 }
@@ -1904,6 +1920,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
       x->n_sm = nsm;
+    x->device = dev;  // the caller's current device owns the tables
   }
   x->NT = d->order + 1;
   x->tab = Tab{d->geo, d->hb, d->nbr, d->ghost, d->hbt, d->ld, d->n_bnd,
@@ -1964,6 +1981,7 @@ int qf_create(const qf_desc* d, qf_ctx** out) {
 
 void qf_destroy(qf_ctx* x) {
   if (!x) return;
+  DevGuard guard(x);
   if (x->graph) cudaGraphExecDestroy(x->graph);
   if (x->vol) cudaFree(x->vol);
   if (x->l2part) cudaFree(x->l2part);
@@ -1973,6 +1991,7 @@ void qf_destroy(qf_ctx* x) {
 
 int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, void* stream) {
   if (!x || !c || !u) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   if (n < 0) {
     e0 = 0;
     n = x->d.n_elem;
@@ -1983,6 +2002,7 @@ int qf_velocity(qf_ctx* x, const double* c, double* u, int32_t e0, int32_t n, vo
 
 int qf_static(qf_ctx* x, int32_t n, void* stream) {
   if (!x) return fail(QF_E_ARG, "null ctx");
+  DevGuard guard(x);
   QF_DISPATCH(x->d.order, launch_static, x, n, (cudaStream_t)stream);
   return cuda_check("static_kernel");
 }
@@ -1990,6 +2010,7 @@ int qf_static(qf_ctx* x, int32_t n, void* stream) {
 int qf_project(qf_ctx* x, const double* prog, int32_t n, double h_min, double* c, double* hb,
                void* stream) {
   if (!x || !prog || !c || !hb) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   x->stream_hint = (cudaStream_t)stream;
   QF_DISPATCH(x->d.order, launch_project, x, prog, n, h_min, c, hb);
   QF_DISPATCH(x->d.order, launch_static, x, n, (cudaStream_t)stream);
@@ -1999,6 +2020,7 @@ int qf_project(qf_ctx* x, const double* prog, int32_t n, double h_min, double* c
 int qf_l2_error(qf_ctx* x, const double* c, double t, int32_t e0, int32_t n, double* sq,
                 void* stream) {
   if (!x || !c || !sq) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   if (x->phys.kind == SCN_NONE) return fail(QF_E_ARG, "scenario has no device exact solution");
   if (n < 0) {
     e0 = 0;
@@ -2019,6 +2041,7 @@ int qf_l2_error(qf_ctx* x, const double* c, double t, int32_t e0, int32_t n, dou
 
 int qf_ghost(qf_ctx* x, double t, void* stream) {
   if (!x) return fail(QF_E_ARG, "null ctx");
+  DevGuard guard(x);
   QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 1, make_double3(0.0, 0.0, 0.0),
               (cudaStream_t)stream);
   return cuda_check("ghost_kernel");
@@ -2031,7 +2054,13 @@ int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms,
 
 int qf_rhs_mass(qf_ctx* x, const double* c, const double* u, double t, int32_t terms,
                 double* rhs, double* lam, double* mflux, void* stream) {
+  return qf_rhs_ex(x, c, u, t, terms, rhs, lam, mflux, nullptr, stream);
+}
+
+int qf_rhs_ex(qf_ctx* x, const double* c, const double* u, double t, int32_t terms, double* rhs,
+              double* lam, double* mflux, const double* lam_in, void* stream) {
   if (!x || !c || !u || !rhs) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   cudaStream_t s = (cudaStream_t)stream;
   if (terms & TERM_EDGE)
     QF_DISPATCH(x->d.order, launch_ghost, x, t, nullptr, 1, make_double3(0.0, 0.0, 0.0), s);
@@ -2041,6 +2070,7 @@ int qf_rhs_mass(qf_ctx* x, const double* c, const double* u, double t, int32_t t
   a.c_out = rhs;
   a.lam = lam;
   a.mflux = (terms & TERM_EDGE) ? mflux : nullptr;
+  a.lam_in = lam_in;
   a.err = x->err;
   a.t = t;
   a.e0 = 0;
@@ -2063,6 +2093,7 @@ int qf_stage_push(qf_ctx* x, const double* c_in, const double* u_in, const doubl
                   const double* t_dev, double toff, int32_t e0, int32_t n, const int32_t* push,
                   const qf_peer* peers, void* stream) {
   if (!x || !c_in || !u_in || !c_out || !u_out) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   if (push && !peers) return fail(QF_E_ARG, "push table without peer table");
   if (aa != 0.0 && !c0) return fail(QF_E_ARG, "stage base c0 required");
   if (n < 0) {
@@ -2126,7 +2157,10 @@ static void step_impl(qf_ctx* x, double* c, double* u, double* work, double* t_d
     A.n = x->d.n_elem;
     A.terms = TERM_VOL | TERM_EDGE | TERM_SRC;
     A.mode = 1;
+    const int si = A.gstage;
+    if (2 * si + 1 < x->n_stage_ev) cudaEventRecordWithFlags(x->stage_ev[2 * si], s, cudaEventRecordExternal);
     QF_DISPATCH(k, launch_stage, x, A, s);
+    if (2 * si + 1 < x->n_stage_ev) cudaEventRecordWithFlags(x->stage_ev[2 * si + 1], s, cudaEventRecordExternal);
   };
   // SSP-RK by order (solver.py:756-764); the last stage writes in place:
   // each thread reads c0[e] before writing c_out[e] and no thread reads
@@ -2151,6 +2185,7 @@ extern "C" {
 
 int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* stream) {
   if (!x || !c || !u || !work || !t_dev) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   step_impl(x, c, u, work, t_dev, (cudaStream_t)stream);
   return cuda_check("qf_step");
 }
@@ -2164,6 +2199,7 @@ static int kernels_per_step(qf_ctx* x) {
 int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, double* t_dev,
            int32_t use_graph, void* stream) {
   if (!x || !c || !u || !work || !t_dev) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   cudaStream_t s = (cudaStream_t)stream;
   if (!use_graph || x->d.order == 0) {
     for (int i = 0; i < n_steps; ++i) step_impl(x, c, u, work, t_dev, s);
@@ -2202,8 +2238,20 @@ int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, doubl
   return cuda_check("qf_run");
 }
 
+int qf_stage_events(qf_ctx* x, void* const* events, int32_t n) {
+  if (!x || n < 0 || n > 8 || (n > 0 && !events)) return fail(QF_E_ARG, "bad stage event list");
+  for (int i = 0; i < n; ++i) x->stage_ev[i] = (cudaEvent_t)events[i];
+  x->n_stage_ev = n;
+  if (x->graph) {  // re-capture with (or without) the event-record nodes
+    cudaGraphExecDestroy(x->graph);
+    x->graph = nullptr;
+  }
+  return QF_OK;
+}
+
 int qf_error(qf_ctx* x, uint32_t* bits, int32_t clear, void* stream) {
   if (!x || !bits) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
   cudaStream_t s = (cudaStream_t)stream;
   unsigned h = 0;
   if (cudaMemcpyAsync(&h, x->err, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||

@@ -103,6 +103,8 @@ class Scenario:
     device: DeviceScenario = field(default_factory=DeviceScenario)
 
     bump_params: dict | None = None          # drawn bump/mode parameters (bump_scenario)
+    # what the device family was built from (a field, so dataclasses.replace keeps it)
+    _device_sig: tuple | None = field(default=None, repr=False, compare=False)
 
     def field_program(self) -> np.ndarray | None:
         """Device field program for qf_project (csrc/qf_kernels.cu), or None."""
@@ -115,6 +117,29 @@ class Scenario:
         if self.device.kind != KIND_NONE and self.initial is None:
             return np.zeros(6)
         return None
+
+    def _physics_signature(self) -> tuple:
+        """The callables and constants a device descriptor was built from."""
+        return (self.hb, self.exact, self.forcing, self.mass_source, float(self.g),
+                float(self.tau_bf), float(self.f_c))
+
+    def _bind_device(self, dev: "DeviceScenario") -> None:
+        """Attach a closed-form device family and record what it was built
+        from (see ``device_matches``)."""
+        self.device = dev
+        self._device_sig = self._physics_signature()
+
+    def device_matches(self) -> bool:
+        """False when ``hb`` / ``exact`` / ``forcing`` / ``mass_source`` / g /
+        tau_bf / f_c were changed after the family factory built the device
+        descriptor (the reference itself assigns ``scn.exact`` / ``scn.forcing``
+        after construction): the kernels would then evaluate other physics
+        than the host callables."""
+        sig = self._device_sig
+        if sig is None:
+            return self.device.kind == KIND_NONE
+        cur = self._physics_signature()
+        return all(a is b for a, b in zip(sig[:4], cur[:4])) and sig[4:] == cur[4:]
 
     def exact_with_velocity(self, x, y, t):
         """Analytic (xi, U, V, u, v); u = U/H with H = hb + xi."""
@@ -198,8 +223,8 @@ def mms_scenario(amp_xi: float = 0.01, amp_u: float = 0.1, amp_v: float = 0.1,
 
     scn.forcing = forcing
     scn.mass_source = mass_source
-    scn.device = DeviceScenario(KIND_MMS, tuple(hb_coeffs) + (amp_xi, amp_u, amp_v),
-                                has_forcing=True)
+    scn._bind_device(DeviceScenario(KIND_MMS, tuple(hb_coeffs) + (amp_xi, amp_u, amp_v),
+                                     has_forcing=True))
     return scn
 
 
@@ -241,7 +266,7 @@ def _travel_scenario(name: str, **kw) -> Scenario:
 
     scn.exact = exact
     scn.forcing = forcing
-    scn.device = DeviceScenario(KIND_TRAVEL, hbp + (Ca, Ct, ya, 0.0), has_forcing=True)
+    scn._bind_device(DeviceScenario(KIND_TRAVEL, hbp + (Ca, Ct, ya, 0.0), has_forcing=True))
     return scn
 
 
@@ -266,7 +291,7 @@ def lake_at_rest_scenario(xi0: float = 0.5, slope=(0.001, 0.002),
 
     scn.exact = exact
     scn.forcing = None
-    scn.device = DeviceScenario(KIND_LAKE, hbp + (float(xi0), 0.0, 0.0, 0.0))
+    scn._bind_device(DeviceScenario(KIND_LAKE, hbp + (float(xi0), 0.0, 0.0, 0.0)))
     return scn
 
 

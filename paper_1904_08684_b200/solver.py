@@ -120,6 +120,19 @@ class DeviceState:
         return DeviceState(self.c.clone(), self.u.clone(), self.t_dev.clone())
 
 
+def _on_device(fn):
+    """Run a Discretization method with its CUDA device current (torch
+    allocations, library launches without a context and the context's own
+    entry points all agree on the device)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrap(self, *a, **kw):
+        with self.torch.cuda.device(self.device):
+            return fn(self, *a, **kw)
+    return wrap
+
+
 def _torch():
     import torch
 
@@ -204,6 +217,11 @@ class HostSetup:
         self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
                                    slots, self.n_own)
         self.h_min = self.tables.h_min
+        if not scenario.device_matches():
+            raise ValueError(f"scenario {scenario.name!r}: hb / exact / forcing / mass_source / g / "
+                             "tau_bf / f_c were changed after its device family was built; the "
+                             "kernels would evaluate different physics than the host callables "
+                             "(build a new scenario instead)")
         needs_data = len(self.tables.bnd_elem) > 0 or scenario.forcing is not None \
             or scenario.mass_source is not None
         if needs_data and scenario.device.kind == KIND_NONE:
@@ -218,7 +236,7 @@ class HostSetup:
         self.dt = scenario.dt
         self._dt_fixed = scenario.cfl is None
         self.phi_at_vertices = np.array(
-            [[f.eval(*v) for v in ((0.0, 0.0), (1.0, 0.0), (0.0, 1.0))]
+            [[f.eval_point(*v) for v in ((0.0, 0.0), (1.0, 0.0), (0.0, 1.0))]
              for f in self.basis.functions])
 
     # ------------------------------------------------------------- setup
@@ -299,6 +317,13 @@ class Discretization(HostSetup):
         torch = _torch()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._pin_in = None      # persistent pinned staging of host State.c uploads
+        self._pin_in_ev = None   # its last H2D (the buffer is reused after it completes)
+        with torch.cuda.device(self.device):
+            self._setup_device_tables()
+
+    def _setup_device_tables(self):
+        torch = self.torch
         lib = _cabi.load()
         tb = self.tables
         E, ld = tb.n_elem, tb.ld
@@ -414,6 +439,7 @@ class Discretization(HostSetup):
             raise ValueError("permuted layout needs full-length host arrays")
         return self._perm.data_ptr()
 
+    @_on_device
     def upload_fields(self, arr: np.ndarray):
         """(n, F, K) host array (n <= local elements) -> device SoA [F][K][ld]."""
         t = self.torch
@@ -429,18 +455,39 @@ class Discretization(HostSetup):
         return (t.empty((3, self.K, self.ld), dtype=t.float64, device=self.device),
                 t.empty((2, self.K, self.ld), dtype=t.float64, device=self.device))
 
+    def _pinned_host(self, c_host: np.ndarray):
+        """A pinned host tensor holding ``c_host``: the array itself when it
+        already lives in page-locked memory (States returned by this class
+        are), else a copy in the persistent staging buffer (no per-call
+        page-locking)."""
+        t = self.torch
+        h = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64))
+        if h.is_pinned():
+            return h
+        if self._pin_in is None or self._pin_in.shape != h.shape:
+            self._pin_in = t.empty(h.shape, dtype=t.float64, pin_memory=True)
+            self._pin_in_ev = None
+        if self._pin_in_ev is not None:
+            self._pin_in_ev.synchronize()  # previous upload from the buffer has finished
+        self._pin_in.copy_(h)
+        return self._pin_in
+
+    @_on_device
     def _upload_c(self, c_host: np.ndarray):
         t = self.torch
         E = len(c_host)
-        # torch's caching host allocator keeps the pinned staging buffer
-        a = t.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64)).pin_memory()
-        a = a.to(self.device, non_blocking=True)
+        h = self._pinned_host(c_host)
+        a = h.to(self.device, non_blocking=True)
+        if h is self._pin_in:
+            self._pin_in_ev = t.cuda.Event()
+            self._pin_in_ev.record(t.cuda.current_stream(self.device))
         c, _ = self._empty_state()
         c.zero_()
         _cabi.check(self._lib.qf_pack(a.data_ptr(), c.data_ptr(), E, a.shape[1], self.K, self.ld,
                                       self._perm_ptr(E), self._stream), "qf_pack")
         return c
 
+    @_on_device
     def _download(self, ds: DeviceState):
         t = self.torch
         E = self.tables.n_elem
@@ -452,8 +499,17 @@ class Discretization(HostSetup):
                                         s), "qf_unpack")
         _cabi.check(self._lib.qf_unpack(ds.u.data_ptr(), ua.data_ptr(), E, 2, self.K, self.ld, pp,
                                         s), "qf_unpack")
-        return ca.cpu().numpy(), ua.cpu().numpy()
+        # page-locked destinations (torch's caching host allocator recycles
+        # them once the arrays are dropped): one async D2H each, one sync; the
+        # returned arrays are caller-owned and feed the next upload directly
+        hc = t.empty(ca.shape, dtype=t.float64, pin_memory=True)
+        hu = t.empty(ua.shape, dtype=t.float64, pin_memory=True)
+        hc.copy_(ca, non_blocking=True)
+        hu.copy_(ua, non_blocking=True)
+        t.cuda.current_stream(self.device).synchronize()
+        return hc.numpy(), hu.numpy()
 
+    @_on_device
     def _soa_to_host(self, x, F):
         t = self.torch
         E = self.tables.n_elem
@@ -462,6 +518,7 @@ class Discretization(HostSetup):
                                         self._perm_ptr(E), self._stream), "qf_unpack")
         return a.cpu().numpy()
 
+    @_on_device
     def to_device(self, state: State, solve: bool = True) -> DeviceState:
         """Device copy of ``state`` (re-used when the state came from the device)."""
         if state._dev is not None and state._c is None and state._dev[0] is self:
@@ -478,6 +535,7 @@ class Discretization(HostSetup):
     def _check(self, status, what):
         _cabi.check(status, what)
 
+    @_on_device
     def _raise_errors(self, where: str):
         bits = _cabi.C.c_uint32(0)
         _cabi.check(self._lib.qf_error(self._ctx, _cabi.C.byref(bits), 1, self._stream),
@@ -496,6 +554,7 @@ class Discretization(HostSetup):
         vals = fn(x, y) if t is None else fn(x, y, t)
         return self.geom.sqrt_detB[:, None] * ((vals * self.quad_w) @ self.quad_phi.T)
 
+    @_on_device
     def _device_initial(self) -> DeviceState:
         c = self._c_init.clone()
         _, u = self._empty_state()
@@ -505,6 +564,7 @@ class Discretization(HostSetup):
         tdev = self.torch.tensor([0.0, self.dt], dtype=self.torch.float64, device=self.device)
         return DeviceState(c, u, tdev)
 
+    @_on_device
     def lambda_max(self, ds: DeviceState, t: float = 0.0) -> float:
         """max over owned element edges of the LF speed of a device state."""
         lam = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device)
@@ -514,6 +574,7 @@ class Discretization(HostSetup):
         self._raise_errors("lambda")
         return float(lam[:, : self.n_own].max().item())
 
+    @_on_device
     def project_initial(self) -> State:
         """Project analytic (or non-analytic ``initial``) data at t = 0 (solver.py:288-303)."""
         if self.device_setup:
@@ -538,6 +599,7 @@ class Discretization(HostSetup):
         return cfl_time_step(self.scn.cfl, self.k, self.h_min, float(lam.max()))
 
     # --------------------------------------------------------- operators
+    @_on_device
     def solve_velocity(self, state: State) -> None:
         """Per-element H-weighted projection solve, in place on state.u (solver.py:315-336)."""
         c = self._upload_c(state.c)
@@ -547,7 +609,25 @@ class Discretization(HostSetup):
         self._raise_errors("solve_velocity")
         state.u[:] = self._soa_to_host(u, 2)
 
-    def _rhs_terms(self, state: State, t: float, terms: int, want_lam=False):
+    @_on_device
+    def _lam_slots(self, lam: np.ndarray):
+        """Per-edge lambda in ``mesh.edges`` order -> device [3][ld] per
+        (local edge, element slot), both sides of an interior edge alike."""
+        lam = np.asarray(lam, dtype=np.float64)
+        cn = self.mesh.conn
+        if self.partitioned or lam.shape != (len(cn.left),):
+            raise ValueError("lam must hold one value per mesh edge (mesh.edges order)")
+        rows = np.zeros((3, self.mesh.n_triangles))
+        rows[cn.left_local, cn.left] = lam
+        inner = cn.right >= 0
+        rows[cn.right_local[inner], cn.right[inner]] = lam[inner]
+        if self.perm is not None:
+            rows = rows[:, self.perm]
+        out = np.zeros((3, self.ld))
+        out[:, : rows.shape[1]] = rows
+        return self.torch.from_numpy(out).to(self.device)
+
+    def _rhs_terms(self, state: State, t: float, terms: int, want_lam=False, lam_in=None):
         c = self._upload_c(state.c)
         _, u = self._empty_state()
         u.zero_()
@@ -562,10 +642,12 @@ class Discretization(HostSetup):
         mass = self.instrument_mass_flux and (terms & _cabi.TERM_EDGE) and not self.partitioned
         mf = self.torch.zeros((3, self.ld), dtype=self.torch.float64, device=self.device) \
             if mass else None
-        self._check(self._lib.qf_rhs_mass(self._ctx, c.data_ptr(), u.data_ptr(), float(t), terms,
-                                          out.data_ptr(), lam.data_ptr() if want_lam else None,
-                                          mf.data_ptr() if mass else None, self._stream),
-                    "qf_rhs_mass")
+        li = None if lam_in is None else self._lam_slots(lam_in)
+        self._check(self._lib.qf_rhs_ex(self._ctx, c.data_ptr(), u.data_ptr(), float(t), terms,
+                                        out.data_ptr(), lam.data_ptr() if want_lam else None,
+                                        mf.data_ptr() if mass else None,
+                                        None if li is None else li.data_ptr(), self._stream),
+                    "qf_rhs_ex")
         self._raise_errors("rhs")
         r = self._soa_to_host(out, 3)
         if mass:
@@ -604,9 +686,10 @@ class Discretization(HostSetup):
         return self._rhs_terms(state, 0.0, _cabi.TERM_VOLUME)
 
     def edge_rhs(self, state: State, t: float, lam: np.ndarray | None = None) -> np.ndarray:
-        """Edge terms; ``lam`` is accepted for signature compatibility (the
-        kernel recomputes the identical per-edge lambda on the device)."""
-        return self._rhs_terms(state, t, _cabi.TERM_EDGE)
+        """Edge terms (solver.py:690-706); a given ``lam`` (per edge, mesh.edges
+        order, as compute_lambda returns it) is used in the Lax-Friedrichs
+        flux instead of the recomputed one, like the reference."""
+        return self._rhs_terms(state, t, _cabi.TERM_EDGE, lam_in=lam)
 
     def source_rhs(self, state: State, t: float) -> np.ndarray:
         return self._rhs_terms(state, t, _cabi.TERM_SOURCE)
@@ -625,6 +708,7 @@ class Discretization(HostSetup):
             self._cfl_warned = True
 
     # ------------------------------------------------------ time stepping
+    @_on_device
     def l2_error_sq(self, state, t: float) -> np.ndarray:
         """Squared L2 errors (xi, U, V) of the owned elements against the
         scenario's exact solution at t, evaluated on the device (qf_l2_error;
@@ -641,6 +725,7 @@ class Discretization(HostSetup):
                                           device=self.device)
         return self._work
 
+    @_on_device
     def step_device(self, ds: DeviceState, n_steps: int = 1, use_graph: bool = True) -> None:
         """Advance a device state in place by n_steps (no host traffic)."""
         w = self._work_buf()
@@ -654,6 +739,7 @@ class Discretization(HostSetup):
                                   self._stream)
             self._check(st, "qf_run")
 
+    @_on_device
     def step(self, state: State) -> State:
         """One SSP-RK step; returns a new State, input unchanged (solver.py:745-770)."""
         ds = self.to_device(state).clone() if state._dev is not None else self.to_device(state)
@@ -665,6 +751,7 @@ class Discretization(HostSetup):
         self._raise_errors(f"step to t = {state.t + self.dt}")
         return State(t=state.t + self.dt, _dev=(self, ds))
 
+    @_on_device
     def run(self, state: State | None = None, t_end: float | None = None) -> State:
         if state is None:
             state = self.project_initial()

@@ -155,6 +155,12 @@ class RootPoly:
             acc = acc + float(c) * x1**a * x2**b
         return acc * math.sqrt(self.rad)
 
+    def eval_point(self, x1: float, x2: float) -> float:
+        """Scalar evaluation with the reference's rounding sequence (a sum of
+        float(coefficient) * x1^a * x2^b, symbolic.py:232-233), so point
+        tables such as ``phi_at_vertices`` match the reference bit for bit."""
+        return sum(exact_float(c, self.rad) * x1**a * x2**b for (a, b), c in self.coef)
+
 
 def _paper_basis() -> list[RootPoly]:
     """The paper's k <= 3 basis, PAPER.md:276-298 (reference symbolic.py:420-435)."""

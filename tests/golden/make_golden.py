@@ -88,6 +88,177 @@ def mms_discretization(R):
     return MassSourceDiscretization
 
 
+def wall_discretization(R):
+    """Oracle extension for the BASELINE C3-C5 physics: every boundary edge
+    is a reflective wall.
+
+    * The wall marker is admitted past the Dirichlet-only check of
+      ``_setup_edges`` (solver.py:174-179) by handing the reference a
+      scenario whose ``dirichlet_markers`` contain it; the boundary pass
+      (``pass_B``) is then built as usual and only its use changes.
+    * ``_boundary_flux`` (solver.py:622-688): the ghost state is the mirror
+      image of the own state, xi+ = xi-, q+ = q- - 2 (q-.n) n, u+ likewise.
+      The normal is constant along a straight edge, so the mirrored
+      coefficient vectors have exactly the mirrored traces; the LF flux is
+      then assembled with the reference's own pair/triple primitives and
+      scalings, the ghost using the element's own h_b (as the Dirichlet
+      ghost does, solver.py:668).
+    * ``compute_lambda`` boundary branch (solver.py:374-405): the mirror has
+      the same depth and |u.n|, so the wall edge's speed is the own side's
+      maximum; DryState when the own depth is non-positive.
+    """
+    import dataclasses
+
+    XI, U, V = 0, 1, 2
+
+    class WallDiscretization(R.solver.Discretization):
+        def compute_lambda(self, state, t):
+            pb = self.pass_B
+            self.pass_B = dataclasses.replace(pb, edge_index=pb.edge_index[:0])
+            try:
+                lam = super().compute_lambda(state, t)
+            finally:
+                self.pass_B = pb
+            g, sd = self.scn.g, self.geom.sqrt_detB
+            for e_t, rows in pb.groups.items():
+                el = pb.elem[rows]
+                tr = self.trace_at_samples[e_t]
+                s = sd[el][:, None]
+                H = ((self.hb_coef[el] + state.c[el, XI]) @ tr) / s
+                un = ((state.u[el, 0] @ tr) * pb.n1[rows, None]
+                      + (state.u[el, 1] @ tr) * pb.n2[rows, None]) / s
+                if (H <= 0.0).any():
+                    raise R.solver.DryState("non-positive depth at a wall edge sample")
+                lam[pb.edge_index[rows]] = (np.abs(un) + np.sqrt(g * H)).max(axis=1)
+            return lam
+
+        def _boundary_flux(self, state, t, lam, rhs):
+            assert self.scn.hb_mode == "linear"
+            pb = self.pass_B
+            g, sd, det = self.scn.g, self.geom.sqrt_detB, self.geom.detB
+            c, u, hb = state.c, state.u, self.hb_coef
+            for e_t, rows in pb.groups.items():
+                ec = pb.elem[rows]
+                n1, n2 = pb.n1[rows][:, None], pb.n2[rows][:, None]
+                ln = pb.length[rows][:, None]
+                lm = lam[pb.edge_index[rows]][:, None]
+
+                def mirror(a, b):
+                    dn = n1 * a + n2 * b
+                    return a - 2.0 * n1 * dn, b - 2.0 * n2 * dn
+
+                own = (c[ec, XI], c[ec, U], c[ec, V], u[ec, 0], u[ec, 1])
+                ghost = (c[ec, XI], *mirror(c[ec, U], c[ec, V]), *mirror(u[ec, 0], u[ec, 1]))
+                ip = (1.0 / det[ec])[:, None]
+                it = (1.0 / (det[ec] * sd[ec]))[:, None]
+                lin, quad = [], []
+                for xi, qx, qy, vx, vy in (own, ghost):
+                    lin.append([self._pair_own(e_t, f) * ip for f in (xi, qx, qy)])
+                    pres = [(xi, xi, 0.5 * g), (xi, hb[ec], g)]
+                    quad.append([
+                        self._triple_own(e_t, [(qx, vx, 1.0)] + pres) * it,
+                        self._triple_own(e_t, [(qx, vy, 1.0)]) * it,
+                        self._triple_own(e_t, [(qy, vx, 1.0)]) * it,
+                        self._triple_own(e_t, [(qy, vy, 1.0)] + pres) * it,
+                    ])
+                (xo, Uo, Vo), (xg, Ug, Vg) = lin
+                A, B_, C_, D = (quad[0][i] + quad[1][i] for i in range(4))
+                f_xi = 0.5 * (n1 * (Uo + Ug) + n2 * (Vo + Vg)) + 0.5 * lm * (xo - xg)
+                f_U = 0.5 * (n1 * A + n2 * B_) + 0.5 * lm * (Uo - Ug)
+                f_V = 0.5 * (n1 * C_ + n2 * D) + 0.5 * lm * (Vo - Vg)
+                rhs[ec] -= np.stack([f_xi, f_U, f_V], axis=1) * ln[:, :, None]
+
+    return WallDiscretization
+
+
+def wall_runs(R):
+    """BASELINE C3/C4 physics (bumps at rest, seeded sine bathymetry,
+    reflective walls, CFL time step) and the C2 schedule, run by the
+    reference at reduced N but at the stated step counts:
+
+    * walls_p3_n16.npz : C3 shape, p = 3, uniform N = 16, 500 steps
+    * walls_p2_j16.npz : C4 shape, p = 2, N = 16 jittered 0.2 h (seed 7), 300 steps
+    * mms_p2_n16.npz   : C2 shape, p = 2, N = 16, SSP-RK3, dt = 2e-5, 1000 steps
+
+    The bump / bathymetry callables and the mesh vertices come from this
+    repository's generators (the reference has none for them); the fixture
+    stores the vertices so the test can check the generator reproduces them.
+    dt = 0.1 h_min / ((2k + 1) lambda_max(t = 0)) with the reference's h_min
+    (solver.py:240-246) and wall lambda; the GPU test checks its own dt
+    against the stored one.
+    """
+    import time
+
+    sys.path.insert(0, str(HERE.parent.parent))
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+
+    Wall = wall_discretization(R)
+    xi0, hb, used = S.bump_fields(0)
+    cases = (("walls_p3_n16", 3, M.build_unit_square_mesh(16), 500),
+             ("walls_p2_j16", 2, M.build_unit_square_mesh(16, jitter=0.2, seed=7), 300))
+    for name, k, m, steps in cases:
+        t0 = time.time()
+        mesh = R.mesh.Mesh(vertices=m.vertices.copy(), triangles=m.triangles.copy())
+        R.mesh._build_edges(mesh)
+        scn = R.scenario.Scenario(name="bumps", dt=1.0, dirichlet_markers=frozenset({1}), hb=hb)
+        disc = Wall(mesh, scn, k)
+        c0 = np.zeros((mesh.n_triangles, 3, disc.K))
+        c0[:, 0] = disc.project_volume(xi0)
+        st0 = R.solver.State(c=c0, u=np.zeros((mesh.n_triangles, 2, disc.K)), t=0.0)
+        disc.solve_velocity(st0)
+        lam0 = disc.compute_lambda(st0, 0.0)
+        dt = 0.1 * disc.h_min / ((2 * k + 1) * float(lam0.max()))
+        scn.dt = dt
+        terms = stage_terms(disc, st0, 0.0)
+        st = st0
+        snaps = {}
+        for i in range(1, steps + 1):
+            st = disc.step(st)
+            if i in (1, 10):
+                snaps[f"c{i}"] = st.c
+        np.savez_compressed(HERE / f"{name}.npz", verts=m.vertices, c0=st0.c, u0=st0.u,
+                            cN=st.c, uN=st.u, steps=steps, dt=dt, h_min=disc.h_min, seed=used,
+                            rhs0=disc.rhs(st0, 0.0), **snaps, **terms)
+        print(f"{name}: {steps} steps, dt={dt:.6e}, {time.time() - t0:.1f} s")
+    # C2 schedule at N = 16
+    t0 = time.time()
+    Disc = mms_discretization(R)
+    disc = Disc(unit_square(R, 16), mms_scenario(R, dt=2e-5, t_end=1000 * 2e-5), 2)
+    st0 = disc.project_initial()
+    st = disc.run(st0)
+    err = R.harness.l2_error(disc, st, st.t)
+    np.savez_compressed(HERE / "mms_p2_n16.npz", c0=st0.c, cN=st.c, uN=st.u, t=st.t, steps=1000,
+                        err=np.array(err.errors()))
+    print(f"mms_p2_n16: 1000 steps, {time.time() - t0:.1f} s")
+
+
+def format_files(R):
+    """Files written by the reference's own writers (byte-comparison fixtures,
+    tests/golden/formats/): ``save_mesh`` (mesh.py:285-301) of the perturbed
+    square level 2 and of a jittered unit-square mesh, ``write_vtk``
+    (harness.py:151-189) of the square_k2 perturbed state, and
+    ``ConvergenceTable.to_csv`` (harness.py:57-68) of the sweep_p1 errors."""
+    sys.path.insert(0, str(HERE.parent.parent))
+    from paper_1904_08684_b200 import mesh as M
+
+    out = HERE / "formats"
+    out.mkdir(exist_ok=True)
+    R.mesh.save_mesh(R.mesh.build_square_mesh(2, 0.2, 5), out / "square_l2.mesh")
+    m = M.build_unit_square_mesh(4, jitter=0.2, seed=7)
+    rm = R.mesh.Mesh(vertices=m.vertices.copy(), triangles=m.triangles.copy())
+    R.mesh._build_edges(rm)
+    R.mesh.save_mesh(rm, out / "unit4_jitter.mesh")
+    g = np.load(HERE / "square_k2.npz")
+    disc = R.solver.Discretization(R.mesh.build_square_mesh(3, 0.2, 42),
+                                   R.scenario.perturbed_square_scenario(dt=0.5), 2)
+    R.harness.write_vtk(disc, R.solver.State(c=g["cr"], u=g["ur"], t=0.0), out / "square_k2.vtk")
+    sw = np.load(HERE / "sweep_p1.npz")
+    rows = [R.harness.ErrorReport(order=1, level=int(n), elements=2 * int(n) ** 2,
+                                  err_xi=float(e[0]), err_U=float(e[1]), err_V=float(e[2]))
+            for n, e in zip(sw["n"], sw["err"])]
+    (out / "sweep_p1.csv").write_text(R.harness.ConvergenceTable(rows=rows).to_csv())
+
+
 def stage_terms(disc, state, t):
     lam = disc.compute_lambda(state, t)
     return dict(lam=lam, elem=disc.element_rhs(state), edge=disc.edge_rhs(state, t, lam),
@@ -139,6 +310,10 @@ def main():
         return tensor_files(R)
     if "--mass-flux" in sys.argv:
         return mass_flux(R)
+    if "--walls" in sys.argv:
+        return wall_runs(R)
+    if "--formats" in sys.argv:
+        return format_files(R)
     # A. tensors
     for k in range(4):
         t = R.tensors.build_ref_tensors(k)
