@@ -509,6 +509,11 @@ def main():
                          "together if a peer mapping fails), or NCCL send/recv")
     ap.add_argument("--no-extra", dest="extra", action="store_false",
                     help="skip the per_config lines (the other BASELINE orders)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak (per-GPU mesh fixed, default) or strong (the BASELINE "
+                         "global mesh: C3 N=1024, C5 N=4096, or --n)")
+    ap.add_argument("--partition", default=None, choices=["strips", "blocks"],
+                    help="N > 1 partition layout (default: blocks for c4, else strips)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU runner even at world size 1 (smoke test)")
     args = ap.parse_args()

@@ -50,7 +50,7 @@ enum { QF_BIT_DRY = 1u, QF_BIT_SINGULAR = 2u, QF_BIT_NONFINITE = 4u };
 enum { QF_TERM_VOLUME = 1, QF_TERM_EDGE = 2, QF_TERM_SOURCE = 4, QF_TERM_ALL = 7 };
 
 /* device scenario families (paper_1904_08684_b200/scenario.py) */
-enum { QF_SCN_NONE = 0, QF_SCN_MMS = 1, QF_SCN_TRAVEL = 2, QF_SCN_LAKE = 3 };
+enum { QF_SCN_NONE = 0, QF_SCN_MMS = 1, QF_SCN_TRAVEL = 2, QF_SCN_LAKE = 3, QF_SCN_USER = 4 };
 
 typedef struct qf_desc {
   int32_t order;            /* k in 0..4 */
@@ -202,6 +202,14 @@ int qf_scatter(const double* src, const int32_t* idx, int32_t n_idx, int32_t row
  * over partitions). */
 int qf_l2_error(qf_ctx* ctx, const double* c, double t, int32_t e0, int32_t n, double* sq,
                 void* stream);
+
+/* User scenario (reference custom_scenario, scenario.py:153-157): `image`
+ * is a cubin / fatbin built from the SymPy fields of the scenario (see
+ * csrc/qf_user.cuh) exporting the kernels qf_user_ghost, with the Dirichlet
+ * data in the layout of the built-in families, and, with with_forcing,
+ * qf_user_forcing, the projected momentum forcing rows the stage kernels add.  Replaces the
+ * context's closed-form family for boundary data and forcing. */
+int qf_user_scenario(qf_ctx* ctx, const void* image, size_t size, int32_t with_forcing);
 
 /* Timing hooks (bench.py): events[2i], events[2i+1] (cudaEvent_t, timing
  * enabled) are recorded around RK stage i of every qf_step / qf_run step,

@@ -72,6 +72,31 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def compile_user_module(source: str) -> bytes:
+    """nvcc a user-scenario module (scenario.user_device_source) to an sm_100a
+    cubin; cached per source digest in the temp directory."""
+    import tempfile
+
+    flags = ["-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+             "--expt-relaxed-constexpr", "-I", str(CSRC)]
+    dig = hashlib.sha256((source + " ".join(flags)).encode())
+    for p in sorted(CSRC.glob("*.cuh")) + sorted((CSRC / "generated").glob("*.cuh")):
+        dig.update(p.read_bytes())
+    cache = Path(tempfile.gettempdir()) / "qfswe_user"
+    cache.mkdir(exist_ok=True)
+    out = cache / f"{dig.hexdigest()[:32]}.cubin"
+    if not out.exists():
+        src = cache / f"{dig.hexdigest()[:32]}.cu"
+        src.write_text(source)
+        tmp = out.with_suffix(f".{os.getpid()}.tmp")
+        res = subprocess.run([nvcc(), *flags, "-o", str(tmp), str(src)], capture_output=True,
+                             text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc (user scenario module) failed:\n{res.stderr[-4000:]}")
+        os.replace(tmp, out)
+    return out.read_bytes()
+
+
 if __name__ == "__main__":
     import sys
 

@@ -38,7 +38,7 @@ constexpr double TWO_PI = 6.283185307179586;
 
 enum : unsigned { BIT_DRY = 1u, BIT_SINGULAR = 2u, BIT_NONFINITE = 4u };
 enum : int { TERM_VOL = 1, TERM_EDGE = 2, TERM_SRC = 4 };
-enum : int { SCN_NONE = 0, SCN_MMS = 1, SCN_TRAVEL = 2, SCN_LAKE = 3 };
+enum : int { SCN_NONE = 0, SCN_MMS = 1, SCN_TRAVEL = 2, SCN_LAKE = 3, SCN_USER = 4 };
 
 // static tables, passed by value
 struct Tab {

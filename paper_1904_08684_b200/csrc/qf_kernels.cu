@@ -88,6 +88,7 @@ struct StageArgs {
   double* mflux;                  // stage_kernel<k, true>: [3][ld] xi mode-0 rhs of each edge
   const qf_peer* peers;           // device table of the peers' destination buffers
   const double* lam_in;           // optional caller-supplied lambda [3][ld] (edge_rhs(state, t, lam))
+  const double* frc;              // optional user-scenario forcing rows [2K][ld] (U, V; qf_user.cuh)
 };
 
 // Fused halo exchange ("a trace-producer kernel stores directly
@@ -897,6 +898,10 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
         r[2 * K + i] += __dmul_rn(gy, xi[i]);
       }
     }
+    if (A.frc) {  // user scenario: forcing rows projected by its own module (qf_user.cuh)
+#pragma unroll
+      for (int i = 0; i < 2 * K; ++i) r[K + i] += ldg(A.frc + i * ld + e);
+    }
     if ((V & V_FC) && P.forcing) {  // sqrt(detB) sum_q w_q phi_p(q) F(x_q, t), reference :719-724
       forcing_quad<k, V>(P, T, e, t, B11, B12, B21, B22, sd, su,
                       [&](const double* Pq, double S, double Fx, double Fy) {
@@ -1682,6 +1687,11 @@ struct qf_ctx {
   // inside the captured run graph, as external event-record nodes)
   cudaEvent_t stage_ev[8] = {};
   int n_stage_ev = 0;
+  // user scenario module (qf_user_scenario): Dirichlet data and forcing kernels
+  cudaLibrary_t user_lib = nullptr;
+  cudaKernel_t user_ghost = nullptr;
+  cudaKernel_t user_forcing = nullptr;
+  double* frc = nullptr;  // [2K][ld] forcing rows of the current stage
 };
 
 // makes the context's device current for the duration of an entry point
@@ -1758,6 +1768,17 @@ static void launch_volume(qf_ctx* x, const StageArgs& a, int vg, cudaStream_t s)
 template <int k>
 static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
   StageArgs a = a_in;
+  if (x->user_forcing && ((a.terms & TERM_SRC) || a.mode == 1) && a.n > 0) {
+    Tab tab = x->tab;
+    const double* td = a.t_dev;
+    double t0 = a.t, toff = a.toff;
+    int e0 = a.e0, n = a.n;
+    double* f = x->frc;
+    void* args[] = {&tab, (void*)&td, &t0, &toff, &e0, &n, &f};
+    cudaLaunchKernel((const void*)x->user_forcing, dim3((n + 127) / 128), dim3(128), args, 0, s);
+    g_launches++;
+    a.frc = x->frc;
+  }
   if constexpr (k >= 3) {
     if ((a.terms & TERM_VOL) && a.n > 0) {
       // one launch per input group (separate register allocation per group)
@@ -1869,9 +1890,18 @@ static void launch_ghost(qf_ctx* x, double t, const double* t_dev, int nstage, d
   const int nb = x->d.n_bnd;
   if (nb <= 0) return;
   const int n = nstage * nb * (Ord<k>::NG + 3);
-  ghost_kernel<k><<<(n + 127) / 128, 128, 0, s>>>(x->tab, x->phys, x->d.bnd_elem,
-                                                  x->d.bnd_local, nb, nstage, t, t_dev, toffs,
-                                                  x->d.ghost);
+  if (x->user_ghost) {  // user scenario module, same table layout
+    Tab tab = x->tab;
+    const int* bel = x->d.bnd_elem;
+    const int* blc = x->d.bnd_local;
+    double* gh = x->d.ghost;
+    void* args[] = {&tab, &bel, &blc, (void*)&nb, &nstage, &t, (void*)&t_dev, &toffs, &gh};
+    cudaLaunchKernel((const void*)x->user_ghost, dim3((n + 127) / 128), dim3(128), args, 0, s);
+  } else {
+    ghost_kernel<k><<<(n + 127) / 128, 128, 0, s>>>(x->tab, x->phys, x->d.bnd_elem,
+                                                    x->d.bnd_local, nb, nstage, t, t_dev, toffs,
+                                                    x->d.ghost);
+  }
   g_launches++;
 }
 
@@ -1985,6 +2015,8 @@ void qf_destroy(qf_ctx* x) {
   if (x->graph) cudaGraphExecDestroy(x->graph);
   if (x->vol) cudaFree(x->vol);
   if (x->l2part) cudaFree(x->l2part);
+  if (x->frc) cudaFree(x->frc);
+  if (x->user_lib) cudaLibraryUnload(x->user_lib);
   cudaFree(x->err);
   delete x;
 }
@@ -2021,7 +2053,8 @@ int qf_l2_error(qf_ctx* x, const double* c, double t, int32_t e0, int32_t n, dou
                 void* stream) {
   if (!x || !c || !sq) return fail(QF_E_ARG, "null argument");
   DevGuard guard(x);
-  if (x->phys.kind == SCN_NONE) return fail(QF_E_ARG, "scenario has no device exact solution");
+  if (x->phys.kind == SCN_NONE || x->phys.kind == SCN_USER)
+    return fail(QF_E_ARG, "scenario has no built-in device exact solution");
   if (n < 0) {
     e0 = 0;
     n = x->d.n_elem;
@@ -2236,6 +2269,35 @@ int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, doubl
   }
   g_launches += (uint64_t)n_steps * kernels_per_step(x);
   return cuda_check("qf_run");
+}
+
+int qf_user_scenario(qf_ctx* x, const void* image, size_t size, int32_t with_forcing) {
+  if (!x || !image || size == 0) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
+  (void)size;
+  cudaLibrary_t lib = nullptr;
+  if (cudaLibraryLoadData(&lib, image, nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess)
+    return cuda_check("cudaLibraryLoadData(user scenario)");
+  cudaKernel_t kg = nullptr, kf = nullptr;
+  if (cudaLibraryGetKernel(&kg, lib, "qf_user_ghost") != cudaSuccess ||
+      (with_forcing && cudaLibraryGetKernel(&kf, lib, "qf_user_forcing") != cudaSuccess)) {
+    cudaLibraryUnload(lib);
+    return cuda_check("cudaLibraryGetKernel(user scenario)");
+  }
+  if (with_forcing && !x->frc &&
+      cudaMalloc(&x->frc, sizeof(double) * 2 * x->K * (size_t)x->d.ld) != cudaSuccess) {
+    cudaLibraryUnload(lib);
+    return fail(QF_E_CUDA, "cudaMalloc(user forcing rows) failed");
+  }
+  if (x->user_lib) cudaLibraryUnload(x->user_lib);
+  x->user_lib = lib;
+  x->user_ghost = kg;
+  x->user_forcing = with_forcing ? kf : nullptr;
+  if (x->graph) {
+    cudaGraphExecDestroy(x->graph);
+    x->graph = nullptr;
+  }
+  return QF_OK;
 }
 
 int qf_stage_events(qf_ctx* x, void* const* events, int32_t n) {

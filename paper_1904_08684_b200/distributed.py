@@ -32,7 +32,8 @@ import numpy as np
 
 from .mesh import Mesh
 
-__all__ = ["strip_partition", "block_partition", "range_partition", "Halo", "build_halo",
+__all__ = ["strip_partition", "block_partition", "block_shape", "range_partition", "Halo",
+           "build_halo",
            "HaloExchange", "push_table", "DistributedRunner", "bench_distributed"]
 
 
@@ -521,8 +522,22 @@ class LocalMultiRunner:
         return out
 
 
+# BASELINE strong-scaling meshes (configs[2]: C3 at N = 1024; configs[4]: C5 at N = 4096)
+STRONG_N = {"c3": 1024, "c5": 4096}
+
+
+def block_shape(world: int) -> tuple[int, int]:
+    """px x py rectangles for ``world`` ranks (C4: 8 -> 4 x 2), px >= py."""
+    py = int(math.isqrt(world))
+    while world % py:
+        py -= 1
+    return world // py, py
+
+
 def bench_distributed(args, configs, metric, hooks=None):
-    """Weak scaling: N_rank = N_base^2 elements per GPU, strip partition.
+    """Weak scaling (default: N_rank = N_base^2 elements per GPU) or strong
+    scaling (``--scaling strong``: the BASELINE global mesh at every N);
+    strips, or px x py blocks (``--partition blocks``; default for C4).
     ``hooks`` (from bench.py): ``clocks()`` -> NVML sampler, ``peaks()`` ->
     (HBM GB/s, source), ``alg_bytes(K, r)`` -> algorithmic bytes per element."""
     import json
@@ -535,11 +550,22 @@ def bench_distributed(args, configs, metric, hooks=None):
 
     rank, world = dist.get_rank(), dist.get_world_size()
     k, n0, scen, dt, jit, desc = configs[args.config]
-    n0 = args.n or n0
-    n = int(round(n0 * math.sqrt(world)))
+    scaling = getattr(args, "scaling", "weak")
+    if scaling == "strong":
+        # fixed global problem at every N: C3 N = 1024, C5 N = 4096 (BASELINE), or --n
+        n = args.n or STRONG_N.get(args.config, n0)
+    else:
+        n = int(round((args.n or n0) * math.sqrt(world)))
     mesh = M.build_unit_square_mesh(n, jitter=jit, seed=7) if jit else M.build_unit_square_mesh(n)
     scn = S.mms_scenario(dt=dt) if scen == "mms" else S.bump_scenario(seed=0, cfl=0.1)
-    part = strip_partition(n, world)
+    layout = getattr(args, "partition", None) or ("blocks" if args.config == "c4" else "strips")
+    if layout == "blocks":
+        px, py = block_shape(world)
+        part = block_partition(n, px, py)
+        playout = f"blocks {px}x{py}"
+    else:
+        part = strip_partition(n, world)
+        playout = f"strips x{world}"
     transport = getattr(args, "transport", "nccl")
     run = DistributedRunner(mesh, scn, k, part, rank, world, transport=transport)
     for _ in range(args.warmup):
@@ -594,10 +620,12 @@ def bench_distributed(args, configs, metric, hooks=None):
     if rank == 0:
         line = {"metric": metric, "value": dof / (t_ms * 1e-3), "unit": "DoF-updates/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc + f" weak-scaled to N={n}", "order": k, "n": n,
-                           "elements": mesh.n_triangles, "parallelism": f"strips x{world}",
+                "config": {"workload": desc + (f" strong (fixed N={n})" if scaling == "strong"
+                                               else f" weak-scaled to N={n}"),
+                           "order": k, "n": n, "elements": mesh.n_triangles,
+                           "parallelism": playout,
                            "halo_transport": run.transport,
                            "halo_transport_note": run.transport_note,
                            "l2": "flushed (256 MB write) between timed steps"},

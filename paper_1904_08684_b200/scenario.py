@@ -49,12 +49,14 @@ __all__ = [
     "KIND_MMS",
     "KIND_TRAVEL",
     "KIND_LAKE",
+    "KIND_USER",
+    "user_device_source",
 ]
 
 TWO_PI = 2.0 * math.pi
 
 # device scenario families (must match csrc/qf_scenario.cuh)
-KIND_NONE, KIND_MMS, KIND_TRAVEL, KIND_LAKE = 0, 1, 2, 3
+KIND_NONE, KIND_MMS, KIND_TRAVEL, KIND_LAKE, KIND_USER = 0, 1, 2, 3, 4
 N_PARAMS = 8
 
 
@@ -114,7 +116,7 @@ class Scenario:
             bumps = np.column_stack([bp["A"], bp["sig"], bp["cen"]]).ravel()
             head = [1.0, 1.0, len(bp["ph"]), len(bp["A"]), 1.0, 0.2]
             return np.concatenate([head, modes, bumps]).astype(np.float64)
-        if self.device.kind != KIND_NONE and self.initial is None:
+        if self.device.kind not in (KIND_NONE, KIND_USER) and self.initial is None:
             return np.zeros(6)
         return None
 
@@ -362,31 +364,97 @@ def bump_scenario(seed: int = 0, cfl: float = 0.1, **kw) -> Scenario:
 
 
 def custom_scenario(xi: str, U: str, V: str, hb: str, **kw) -> Scenario:
-    """Scenario from SymPy expression strings (reference scenario.py:153-157).
-
-    The stage kernels only evaluate the closed-form families above, so a
-    custom scenario is accepted only when it needs no device evaluation
-    (no Dirichlet boundary data and no forcing); otherwise ``Discretization``
-    raises ``ValueError``.
+    """Scenario from SymPy expression strings in x, y, t (reference
+    scenario.py:153-157, built like ``_build(..., manufacture=True)``): host
+    callables by ``lambdify``, the momentum forcing manufactured from the
+    fields (reference ``_manufacture``, scenario.py:69-94; ValueError for a
+    non-zero mass residual), and a device description that
+    ``Discretization`` compiles into a per-scenario module
+    (``device_source``, csrc/qf_user.cuh, ``qf_user_scenario``): Dirichlet
+    data and forcing are evaluated on the GPU every stage, like the reference
+    evaluates ``exact_with_velocity`` and ``forcing`` (solver.py:396,637,721).
     """
     import sympy as sp
 
     X, Y, T = sp.symbols("x y t", real=True)
     loc = {"x": X, "y": Y, "t": T}
     ex = [sp.sympify(s, locals=loc) for s in (xi, U, V, hb)]
-    f_exact = [sp.lambdify((X, Y, T), e, modules="numpy") for e in ex[:3]]
-    f_hb = sp.lambdify((X, Y), ex[3], modules="numpy")
     scn = Scenario(name="custom", **kw)
+    xi_e, U_e, V_e, hb_e = ex
+    H = hb_e + xi_e
+    residual = sp.simplify(sp.diff(xi_e, T) + sp.diff(U_e, X) + sp.diff(V_e, Y))
+    if residual != 0:
+        raise ValueError(f"analytic fields violate the sourceless mass equation: residual {residual}")
+    g = sp.Float(scn.g)
+    Fx = (sp.diff(U_e, T) + sp.diff(U_e**2 / H, X) + sp.diff(U_e * V_e / H, Y)
+          + scn.tau_bf * U_e - scn.f_c * V_e + g * H * sp.diff(xi_e, X))
+    Fy = (sp.diff(V_e, T) + sp.diff(U_e * V_e / H, X) + sp.diff(V_e**2 / H, Y)
+          + scn.tau_bf * V_e + scn.f_c * U_e + g * H * sp.diff(xi_e, Y))
 
-    def bc(f, *a):
-        shape = np.broadcast(*[np.asarray(v) for v in a]).shape
-        return np.broadcast_to(np.asarray(f(*a), dtype=float), shape)
+    def lam(args, exprs):
+        fns = [sp.lambdify(args, e, modules="numpy") for e in exprs]
 
-    scn.hb = lambda x, y: bc(f_hb, x, y)
-    scn.exact = lambda x, y, t: tuple(bc(f, x, y, t) for f in f_exact)
-    scn.device = DeviceScenario(KIND_NONE)
+        def call(*vals):
+            shape = np.broadcast(*[np.asarray(v) for v in vals]).shape
+            return tuple(np.broadcast_to(np.asarray(f(*vals), dtype=float), shape) for f in fns)
+        return call
+
+    f_hb = lam((X, Y), [hb_e])
+    scn.hb = lambda x, y: f_hb(x, y)[0]
+    scn.exact = lam((X, Y, T), ex[:3])
+    manufactured = not (Fx == 0 and Fy == 0)
+    scn.forcing = lam((X, Y, T), [Fx, Fy]) if manufactured else None
     scn._custom_exprs = ex  # type: ignore[attr-defined]
+    scn._custom_syms = (X, Y, T)  # type: ignore[attr-defined]
+    scn._custom_forcing = (Fx, Fy) if manufactured else None  # type: ignore[attr-defined]
+    scn._bind_device(DeviceScenario(KIND_USER, has_forcing=manufactured))
     return scn
+
+
+def user_device_source(scn: Scenario, k: int) -> str:
+    """CUDA source of a custom scenario's device module for order k: the
+    SymPy fields printed as C99 (common subexpressions shared), wrapped in
+    the templates of csrc/qf_user.cuh."""
+    import sympy as sp
+    from sympy.printing.c import C99CodePrinter
+
+    pr = C99CodePrinter()
+
+    def body(outs, exprs):
+        reps, red = sp.cse([sp.sympify(e) for e in exprs], symbols=sp.numbered_symbols("q_"))
+        lines = [f"    const double {s} = {pr.doprint(e)};" for s, e in reps]
+        lines += [f"    {o} = {pr.doprint(e)};" for o, e in zip(outs, red)]
+        return "\n".join(lines)
+
+    xi, U, V, hb = scn._custom_exprs
+    F = scn._custom_forcing or (sp.Integer(0), sp.Integer(0))
+    return f"""// generated by paper_1904_08684_b200/scenario.py:user_device_source (k = {k})
+#include <math.h>
+#ifndef M_PI
+#define M_PI 3.141592653589793
+#endif
+#include "qf_device.cuh"
+#include "generated/qf_order{k}.cuh"
+#include "qf_user.cuh"
+struct UserScn {{
+  static __device__ void exact(double x, double y, double t, double& xi, double& U, double& V,
+                               double& hb) {{
+{body(("xi", "U", "V", "hb"), (xi, U, V, hb))}
+  }}
+  static __device__ void forcing(double x, double y, double t, double& Fx, double& Fy) {{
+{body(("Fx", "Fy"), F)}
+  }}
+}};
+extern "C" __global__ void __launch_bounds__(128) qf_user_ghost(
+    qf::Tab T, const int* bel, const int* bloc, int nb, int nstage, double t0,
+    const double* t_dev, double3 toffs, double* ghost) {{
+  qf::user_ghost<{k}, UserScn>(T, bel, bloc, nb, nstage, t0, t_dev, toffs, ghost);
+}}
+extern "C" __global__ void __launch_bounds__(128) qf_user_forcing(
+    qf::Tab T, const double* t_dev, double t0, double toff, int e0, int n, double* frc) {{
+  qf::user_forcing<{k}, UserScn>(T, t_dev, t0, toff, e0, n, frc);
+}}
+"""
 
 
 _SCENARIOS = {

@@ -26,7 +26,7 @@ import numpy as np
 from . import _cabi
 from .layout import BND_DIRICHLET, build_tables, pad_ld
 from .mesh import ElementGeometry, Mesh, compute_geometry, locality_order
-from .scenario import KIND_MMS, KIND_NONE, Scenario
+from .scenario import KIND_MMS, KIND_NONE, KIND_USER, Scenario
 from .symbolic import build_basis
 from .tensors import build_ref_tensors, triangle_rule
 
@@ -356,7 +356,10 @@ class Discretization(HostSetup):
         d.scn_kind = scn.device.kind
         for i, p in enumerate(scn.device.as_array()):
             d.scn_params[i] = float(p)
-        d.has_forcing = 1 if (scn.forcing is not None or scn.mass_source is not None) else 0
+        user = scn.device.kind == KIND_USER
+        # (user scenarios: forcing and boundary data come from their own module)
+        d.has_forcing = 0 if user else \
+            (1 if (scn.forcing is not None or scn.mass_source is not None) else 0)
         # element-local Taylor sin/cos for the MMS phases: 1 = degree 9/8
         # (|z| <= 0.06), 2 = degree 7/6 (|z| <= 0.02); truncation < 1e-18
         ang = self._max_quad_angle()
@@ -370,6 +373,8 @@ class Discretization(HostSetup):
         self._ctx = ctx
         self._lib = lib
         self._work = None
+        if user:
+            self._load_user_module()
         if not self.device_setup:
             self._check(lib.qf_static(ctx, len(self.elements), self._stream), "qf_static")
         if self.device_setup:
@@ -381,6 +386,18 @@ class Discretization(HostSetup):
                                        self._stream), "qf_project")
             self._c_init = c0
             self._raise_errors("initial projection")
+
+    def _load_user_module(self):
+        """Compile and bind the custom scenario's device module (Dirichlet
+        data + manufactured forcing, csrc/qf_user.cuh)."""
+        from .build import compile_user_module
+        from .scenario import user_device_source
+
+        image = compile_user_module(user_device_source(self.scn, self.k))
+        self._user_image = _cabi.C.create_string_buffer(image, len(image))
+        forcing = self.scn.forcing is not None
+        _cabi.check(self._lib.qf_user_scenario(self._ctx, self._user_image, len(image),
+                                               1 if forcing else 0), "qf_user_scenario")
 
     def _uniform_phase_table(self):
         """MMS forcing on a mesh whose element Jacobians take at most two

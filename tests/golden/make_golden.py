@@ -259,6 +259,28 @@ def format_files(R):
     (out / "sweep_p1.csv").write_text(R.harness.ConvergenceTable(rows=rows).to_csv())
 
 
+CUSTOM_FIELDS = ("sin(x/300 - t/10)/100", "0.3*sin(x/300 - t/10) + 0.1", "0.05*cos(x/500)",
+                 "2 + x/2000 + y/3000")
+
+
+def custom_runs(R):
+    """Reference ``custom_scenario`` (scenario.py:153-157; Dirichlet data from
+    the fields, momentum forcing manufactured by SymPy) on the perturbed
+    square, k = 1..3: terms on a perturbed state and 5 steps."""
+    mesh = R.mesh.build_square_mesh(3, 0.2, 42)
+    for k in (1, 2, 3):
+        scn = R.scenario.custom_scenario(*CUSTOM_FIELDS, dt=0.5)
+        disc = R.solver.Discretization(mesh, scn, k)
+        st0 = disc.project_initial()
+        sr = perturbed_state(disc, st0, 500 + k)
+        terms = stage_terms(disc, sr, 2.3)
+        st = st0
+        for _ in range(5):
+            st = disc.step(st)
+        np.savez_compressed(HERE / f"custom_k{k}.npz", c0=st0.c, cr=sr.c, ur=sr.u,
+                            rhs_r=disc.rhs(sr, 2.3), c5=st.c, u5=st.u, **terms)
+
+
 def stage_terms(disc, state, t):
     lam = disc.compute_lambda(state, t)
     return dict(lam=lam, elem=disc.element_rhs(state), edge=disc.edge_rhs(state, t, lam),
@@ -314,6 +336,8 @@ def main():
         return wall_runs(R)
     if "--formats" in sys.argv:
         return format_files(R)
+    if "--custom" in sys.argv:
+        return custom_runs(R)
     # A. tensors
     for k in range(4):
         t = R.tensors.build_ref_tensors(k)
