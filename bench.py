@@ -497,7 +497,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=None, help="override mesh resolution")
+    ap.add_argument("--n", "--mesh-n", dest="n", type=int, default=None,
+                    help="override mesh resolution (--mesh-n under torchrun, whose own "
+                         "options would swallow --n)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true",

@@ -84,13 +84,12 @@ typedef struct qf_desc {
 
 typedef struct qf_ctx qf_ctx;
 
-/* Destination buffers of one peer partition for the fused halo push: its
- * stage-output state c[3][K][ld] and u[2][K][ld] (device pointers: same GPU,
- * peer-accessible, or mapped with qf_ipc_import). */
+/* Destination of the fused halo push in one peer partition: its halo trace
+ * table for the stage output, ht[row][6][k+1] (trace moments of xi, U, V,
+ * u, v, h_b on the cut edge, in the sender's edge parametrisation); device
+ * pointer on the same GPU, peer-accessible, or mapped with qf_ipc_import. */
 typedef struct qf_peer {
-  double* c;
-  double* u;
-  int64_t ld;
+  double* ht;
 } qf_peer;
 
 /* Discretization.__init__ (solver.py:103-124): bind tables, validate. */
@@ -143,18 +142,31 @@ int qf_stage(qf_ctx* ctx, const double* c_in, const double* u_in, const double* 
              double* c_out, double* u_out, double a, double b, double t, double dt,
              const double* t_dev, double toff, int32_t e0, int32_t n, void* stream);
 
-/* qf_stage with the halo exchange fused into the stage (replaces
- * the reference-less gather -> send/recv -> scatter of a partitioned run):
- * the thread that computes a cut-adjacent element's new (c, u) also stores
- * them into the halo slots of the peers that hold it.  push (device int32
- * [3][ld], may be NULL): per element up to three destinations
- * (peer << 26) | peer slot, or -1; peers: device qf_peer table indexed by
- * peer.  Ordering with the peers' next stage is the caller's (stream order
- * on one GPU, qf_signal / qf_wait across processes). */
+/* qf_stage on a partition, with the halo exchange fused into the stage
+ * (SURVEY §8e).  Neighbour codes 4 h + 3 (layout.py) name row h of the
+ * halo trace table ht_in (device, rows of 6 (k+1) doubles: the trace
+ * moments of the other partition's element on the shared edge for the
+ * stage input).  push (device int32 [3][ld], may be NULL): per element and
+ * local cut edge the destination (peer << 26) | row; the thread that
+ * computes a cut-adjacent element's new (c, u) also computes its trace
+ * moments on that edge and stores them into the peer's table (peers: device
+ * qf_peer table indexed by peer).  Ordering with the peers' next stage is
+ * the caller's (stream order on one GPU, qf_signal / qf_wait across
+ * processes). */
 int qf_stage_push(qf_ctx* ctx, const double* c_in, const double* u_in, const double* c0,
                   double* c_out, double* u_out, double a, double b, double t, double dt,
-                  const double* t_dev, double toff, int32_t e0, int32_t n, const int32_t* push,
-                  const qf_peer* peers, void* stream);
+                  const double* t_dev, double toff, int32_t e0, int32_t n, const double* ht_in,
+                  const int32_t* push, const qf_peer* peers, void* stream);
+
+/* Halo trace rows for the NCCL transport: out[i][6][k+1] = trace moments of
+ * element items[i] >> 2 on its local edge items[i] & 3 of state (c, u), with
+ * the stage kernel's rounding (bit-identical to what the fused push stores). */
+int qf_halo_traces(qf_ctx* ctx, const double* c, const double* u, const int32_t* items,
+                   int32_t n, double* out, void* stream);
+
+/* Halo trace table used by qf_rhs / qf_velocity-free operators on a
+ * partition (the stage input of qf_stage_push is explicit); NULL clears. */
+int qf_halo_table(qf_ctx* ctx, const double* ht);
 
 /* Stream-ordered 32-bit flag write (local or peer memory) and wait until
  * (int32)(*flag - value) >= 0: cross-process stage ordering of the fused
@@ -219,6 +231,10 @@ int qf_stage_events(qf_ctx* ctx, void* const* events, int32_t n);
 
 /* Read (and optionally clear) the error word; synchronises `stream`. */
 int qf_error(qf_ctx* ctx, uint32_t* bits, int32_t clear, void* stream);
+
+/* Stream-ordered copy of `bytes` between device buffers (local, peer or
+ * IPC-mapped; the initial halo trace rows of the fused transport). */
+int qf_copy(void* dst, const void* src, size_t bytes, void* stream);
 
 /* Fill n doubles with v (L2 flush for timing). */
 int qf_fill(double* buf, size_t n, double v, void* stream);

@@ -66,6 +66,7 @@ class TraceStage:
     """One RHS / RK stage on SoA tables for elements [0, n_own)."""
 
     def __init__(self, k, geo, nbr, hb, n_own, scn, bnd_elem=None, bnd_local=None):
+        self.ht = np.zeros((0, 6, k + 1))  # halo trace rows of the current stage input
         self.ops = TraceOps(k)
         self.k = k
         self.geo, self.nbr, self.hb, self.n = geo, nbr, hb, n_own
@@ -204,8 +205,10 @@ class TraceStage:
                                hbK], idx, sd)
         code = self.nbr[j, :n].astype(np.int64)
         inner = code >= 0
-        nb = np.where(inner, code >> 2, 0)
-        jn = np.where(inner, code & 3, 0)
+        halo = inner & ((code & 3) == 3)  # other partition's element: row of self.ht
+        hrow = np.where(halo, code >> 2, 0)
+        nb = np.where(inner & ~halo, code >> 2, 0)
+        jn = np.where(inner & ~halo, code & 3, 0)
         v = np.where(inner, 0, -1 - code)
         kind = v & 1
         slot = v >> 1
@@ -214,6 +217,9 @@ class TraceStage:
         hbn = self._hbfull(nb)
         oth = self._traces(jn, [c[0][:, nb], c[1][:, nb], c[2][:, nb], u[0][:, nb], u[1][:, nb],
                                 hbn], nb, sdn)
+        if halo.any():
+            for f in range(6):
+                oth[f][:, halo] = self.ht[hrow[halo], f].T
         oth = [ops.R[:, None] * f for f in oth]
         # boundary ghosts
         bd = ~inner & (kind == 0)
@@ -265,6 +271,17 @@ class TraceStage:
         s = ln / sd
         for f, F in enumerate((Fx, FU, FV)):
             out[f] -= s * (L @ F)
+
+    def halo_traces(self, c, u, items):
+        """Halo trace rows (n, 6, NT) of (element items >> 2, edge items & 3),
+        the neighbour-side traces ``_edge`` computes for in-partition
+        neighbours (the multi-rank CPU tests exchange these)."""
+        items = np.asarray(items, dtype=np.int64)
+        e, j = items >> 2, items & 3
+        sd = self._geom(e)[5]
+        tr = self._traces(j, [c[0][:, e], c[1][:, e], c[2][:, e], u[0][:, e], u[1][:, e],
+                              self._hbfull(e)], e, sd)
+        return np.stack(tr, axis=1).transpose(2, 1, 0)
 
     def stage_coeffs(self, a, b, c_in, u_in, c0, t, dt):
         """c_out = a c0 + b (c_in + dt L(c_in)) for owned elements, and its velocity."""

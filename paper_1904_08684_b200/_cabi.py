@@ -23,7 +23,7 @@ EXPORTS = (
     "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
     "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error", "qf_rhs_mass",
     "qf_stage_push", "qf_signal", "qf_wait", "qf_ipc_export", "qf_ipc_import", "qf_ipc_close_all",
-    "qf_launch_count", "qf_last_error", "qf_abi_version", "qf_stage_events", "qf_rhs_ex", "qf_user_scenario",
+    "qf_launch_count", "qf_last_error", "qf_abi_version", "qf_stage_events", "qf_rhs_ex", "qf_user_scenario", "qf_halo_traces", "qf_halo_table", "qf_copy",
 )
 
 
@@ -74,7 +74,10 @@ def load(path: Path | None = None):
         "qf_fill": (C.c_int, [vp, C.c_size_t, d, vp]),
         "qf_l2_error": (C.c_int, [vp, vp, d, i32, i32, vp, vp]),
         "qf_stage_push": (C.c_int, [vp, vp, vp, vp, vp, vp, d, d, d, d, vp, d, i32, i32, vp, vp,
-                                    vp]),
+                                    vp, vp]),
+        "qf_halo_traces": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+        "qf_halo_table": (C.c_int, [vp, vp]),
+        "qf_copy": (C.c_int, [vp, vp, C.c_size_t, vp]),
         "qf_signal": (C.c_int, [vp, C.c_uint32, vp]),
         "qf_wait": (C.c_int, [vp, C.c_uint32, vp]),
         "qf_ipc_export": (C.c_int, [vp, vp, C.POINTER(C.c_uint64)]),

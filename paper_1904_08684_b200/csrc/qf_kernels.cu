@@ -89,33 +89,64 @@ struct StageArgs {
   const qf_peer* peers;           // device table of the peers' destination buffers
   const double* lam_in;           // optional caller-supplied lambda [3][ld] (edge_rhs(state, t, lam))
   const double* frc;              // optional user-scenario forcing rows [2K][ld] (U, V; qf_user.cuh)
+  const double* ht;               // halo trace table of the stage input (partitions), see HALO_J
 };
 
+// Neighbour code 4 h + HALO_J (a local-edge value no element has): the
+// neighbour is owned by another partition and its trace moments on the
+// shared edge arrive in row h of the halo trace table ht[h][6][NT] (xi, U,
+// V, u, v, h_b in the neighbour's own edge parametrisation), pushed by the
+// peer's stage epilogue or exchanged by qf_halo_traces + NCCL (SURVEY §8e:
+// 6 (k + 1) doubles per cut edge instead of the neighbour's 5 K rows).
+constexpr int HALO_J = 3;
+
+// Trace moments of fields (xi, U, V, u, v) of one element on local edge j
+// with the rounding sequence of the stage kernel's phase A2 (so a partition
+// sees bit-identical neighbour traces), h_b from the static table:
+// out[f * NT + a], f < 6.  c rows at c[i * ld], velocity rows in registers.
+template <int k>
+__device__ __forceinline__ void edge_traces6(const Tab& T, int64_t ld, int e, int j,
+                                             const double* c, const double* uo, const double* vo,
+                                             double* out, int ostride) {
+  using O = Ord<k>;
+  constexpr int K = O::K, NT = O::NT;
+  const double* L = Tabs<k>::ptr() + Tabs<k>::L + j * K * NT;
+  const double nisd = rsqrt_fast(det2(T.geo[e], T.geo[ld + e], T.geo[2 * ld + e], T.geo[3 * ld + e]));
+#pragma unroll 1
+  for (int fi = 0; fi < 5; ++fi) {
+#pragma unroll
+    for (int a = 0; a < NT; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const double f = fi < 3 ? c[(fi * K + i) * ld] : (fi == 3 ? uo[i] : vo[i]);
+        acc = __fma_rn(L[i * NT + a], f, acc);
+      }
+      out[(fi * NT + a) * ostride] = __dmul_rn(acc, nisd);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NT; ++a) out[(5 * NT + a) * ostride] = T.hbt[(j * NT + a) * ld + e];
+}
+
 // Fused halo exchange ("a trace-producer kernel stores directly
-// into the peer's buffer"): a cut-adjacent element's new (c, u) rows are
-// stored by the thread that computed them straight into the halo slots of
-// up to three peer partitions (device pointers: same GPU, P2P or CUDA-IPC
-// mapped over NVLink).  push[j][e] = (peer << 26) | peer slot, or -1.
-// (c is re-read from the row the thread has just written, so no register
-// stays live across the velocity solve)
-template <int K>
-__device__ __forceinline__ void push_rows(const int* __restrict__ push,
-                                          const qf_peer* __restrict__ peers, int64_t ld, int e,
-                                          const double* c_new, const double* uo,
-                                          const double* vo) {
+// into the peer's buffer"): the thread that computed a cut-adjacent
+// element's new (c, u) also computes its trace moments on each cut edge and
+// stores them into the peer's halo trace table (device pointers: same GPU,
+// P2P or CUDA-IPC mapped over NVLink).  push[j][e] = (peer << 26) | row, or -1.
+template <int k>
+__device__ __forceinline__ void push_traces(const Tab& T, const int* __restrict__ push,
+                                            const qf_peer* __restrict__ peers, int64_t ld, int e,
+                                            const double* c_new, const double* uo,
+                                            const double* vo) {
+  constexpr int NT = Ord<k>::NT;
 #pragma unroll 1
   for (int j = 0; j < 3; ++j) {
     const int d = __ldg(push + j * ld + e);
     if (d < 0) continue;
     const qf_peer pr = peers[d >> 26];
-    const int64_t sl = d & ((1 << 26) - 1);
-#pragma unroll
-    for (int i = 0; i < 3 * K; ++i) pr.c[i * pr.ld + sl] = c_new[i * ld + e];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      pr.u[i * pr.ld + sl] = uo[i];
-      pr.u[(K + i) * pr.ld + sl] = vo[i];
-    }
+    const int64_t row = d & ((1 << 26) - 1);
+    edge_traces6<k>(T, ld, e, j, c_new + e, uo, vo, pr.ht + row * 6 * NT, 1);
   }
 }
 
@@ -253,15 +284,17 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
   const double* gp = nullptr;
   if (code >= 0) {
     const int nb = code >> 2, jn = code & 3;
+    const bool halo = jn == HALO_J;  // traces of another partition's element (A.ht row nb)
     if constexpr (!HS) {
 #pragma unroll
       for (int a = 0; a < NT; ++a) {
-        const double v = ldg(T.hbt + (jn * NT + a) * ld + nb);
+        const double v = halo ? ldg(A.ht + (int64_t)nb * 6 * NT + 5 * NT + a)
+                              : ldg(T.hbt + (jn * NT + a) * ld + nb);
         oth[5][a] = (a & 1) ? -v : v;  // s -> 1-s
       }
     }
-    if (!hbl) hbm_n = ldg(T.hbt + 3 * NT * ld + nb);
-    if (nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
+    if (!hbl) hbm_n = halo ? 0.0 : ldg(T.hbt + 3 * NT * ld + nb);
+    if (!halo && nb >= blo && nb < bhi) {  // neighbour traced by its own thread in phase A
       const int ns = nb - blo;
 #pragma unroll
       for (int f = 0; f < NF; ++f)
@@ -276,6 +309,14 @@ __device__ __forceinline__ void edge_flux(const Tab& T, const Phys& P, const Sta
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
           const double v = s_ht[(f * NT + a) * HC + hslot];
+          oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
+        }
+    } else if (halo) {  // request list overflow, halo neighbour: its row of the trace table
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+          const double v = ldg(A.ht + (int64_t)nb * 6 * NT + f * NT + a);
           oth[f][a] = (a & 1) ? -v : v;  // s -> 1-s
         }
     } else {  // request list overflow (rare): gather and trace here, compact code
@@ -738,7 +779,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const int nb = code[j] >> 2;
-      const bool req = active && code[j] >= 0 && (nb < blo || nb >= bhi);
+      const bool req = active && code[j] >= 0 && ((code[j] & 3) == HALO_J || nb < blo || nb >= bhi);
       const unsigned m = __ballot_sync(0xffffffffu, req);
       const int pos = base + __popc(m & ((1u << lane) - 1u));
       if (req && pos < WC) {
@@ -758,9 +799,9 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     hsl = w * WC + le;
   };
   auto a2_trace = [&](int hsl, int fi, const double* f, const double* g4) {
-    if (NF == 6 && fi == 5) {  // static h_b trace of the neighbour: copied
+    if ((NF == 6 && fi == 5) || (s_req[hsl] & 3) == HALO_J) {  // copied (static h_b, halo row)
 #pragma unroll
-      for (int a = 0; a < NT; ++a) s_ht[(5 * NT + a) * HC + hsl] = f[a];
+      for (int a = 0; a < NT; ++a) s_ht[(fi * NT + a) * HC + hsl] = f[a];
       return;
     }
     const int cd = s_req[hsl], jn = cd & 3;
@@ -776,8 +817,13 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   };
   auto a2_load = [&](int hsl, int fi, double* f, double* g4) {
     const int nb = s_req[hsl] >> 2;
+    const int jn = s_req[hsl] & 3;
+    if (jn == HALO_J) {  // row nb of the halo trace table (another partition's element)
+#pragma unroll
+      for (int a = 0; a < NT; ++a) f[a] = ldg(A.ht + (int64_t)nb * 6 * NT + fi * NT + a);
+      return;
+    }
     if (NF == 6 && fi == 5) {
-      const int jn = s_req[hsl] & 3;
 #pragma unroll
       for (int a = 0; a < NT; ++a) f[a] = ldg(T.hbt + (jn * NT + a) * ld + nb);
       return;
@@ -949,7 +995,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     A.u_out[(K + i) * ld + e] = vo[i];
   }
   if constexpr ((V & V_PUSH) != 0) {
-    if (A.push) push_rows<K>(A.push, A.peers, ld, e, A.c_out, uo, vo);
+    if (A.push) push_traces<k>(T, A.push, A.peers, ld, e, A.c_out, uo, vo);
   }
 }
 
@@ -1343,7 +1389,7 @@ __global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : (k == 3 ? QF_VELOCC
     u[i * ld + e] = uo[i];
     u[(K + i) * ld + e] = vo[i];
   }
-  if constexpr (PUSH) push_rows<K>(push, peers, ld, e, c, uo, vo);
+  if constexpr (PUSH) push_traces<k>(T, push, peers, ld, e, c, uo, vo);
 }
 
 // Dirichlet ghost data: exact (xi, U, V, u, v) at the k+2 Gauss points of
@@ -1588,6 +1634,24 @@ __global__ void __launch_bounds__(L2_BS) l2sum_kernel(const double* __restrict__
 
 __global__ void advance_time(double* t_dev) { t_dev[0] += t_dev[1]; }
 
+// halo trace rows out[i][6][NT] of (element items[i] >> 2, local edge items[i] & 3)
+template <int k>
+__global__ void halo_trace_kernel(Tab T, const double* __restrict__ c, const double* __restrict__ u,
+                                  const int* __restrict__ items, int n, double* __restrict__ out) {
+  constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int e = items[i] >> 2, j = items[i] & 3;
+  const int64_t ld = T.ld;
+  double uo[K], vo[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    uo[p] = u[p * ld + e];
+    vo[p] = u[(K + p) * ld + e];
+  }
+  edge_traces6<k>(T, ld, e, j, c + e, uo, vo, out + (int64_t)i * 6 * NT, 1);
+}
+
 __global__ void pack_kernel(const double* __restrict__ aos, double* __restrict__ soa, int n, int F,
                             int K, int64_t ld, const int* __restrict__ perm) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1639,7 +1703,7 @@ __global__ void request_count_kernel(const int* __restrict__ nbr, int64_t ld, in
   if (e < n) {
     for (int j = 0; j < 3; ++j) {
       const int code = nbr[j * ld + e], nb = code >> 2;
-      c += code >= 0 && (nb < blo || nb >= bhi);
+      c += code >= 0 && ((code & 3) == qf::HALO_J || nb < blo || nb >= bhi);
     }
   }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -1692,6 +1756,7 @@ struct qf_ctx {
   cudaKernel_t user_ghost = nullptr;
   cudaKernel_t user_forcing = nullptr;
   double* frc = nullptr;  // [2K][ld] forcing rows of the current stage
+  const double* halo_ht = nullptr;  // halo trace table for qf_rhs / qf_stage (partitions)
 };
 
 // makes the context's device current for the duration of an entry point
@@ -1929,6 +1994,13 @@ static void launch_l2(qf_ctx* x, const double* c, double t, int e0, int n, int n
   g_launches += 2;
 }
 
+template <int k>
+static void launch_halo_traces(qf_ctx* x, const double* c, const double* u, const int32_t* items,
+                               int n, double* out, cudaStream_t s) {
+  halo_trace_kernel<k><<<(n + 127) / 128, 128, 0, s>>>(x->tab, c, u, items, n, out);
+  g_launches++;
+}
+
 extern "C" {
 
 int qf_abi_version(void) { return 2; }
@@ -2104,6 +2176,7 @@ int qf_rhs_ex(qf_ctx* x, const double* c, const double* u, double t, int32_t ter
   a.lam = lam;
   a.mflux = (terms & TERM_EDGE) ? mflux : nullptr;
   a.lam_in = lam_in;
+  a.ht = x->halo_ht;
   a.err = x->err;
   a.t = t;
   a.e0 = 0;
@@ -2117,14 +2190,14 @@ int qf_rhs_ex(qf_ctx* x, const double* c, const double* u, double t, int32_t ter
 int qf_stage(qf_ctx* x, const double* c_in, const double* u_in, const double* c0, double* c_out,
              double* u_out, double aa, double bb, double t, double dt, const double* t_dev,
              double toff, int32_t e0, int32_t n, void* stream) {
-  return qf_stage_push(x, c_in, u_in, c0, c_out, u_out, aa, bb, t, dt, t_dev, toff, e0, n, nullptr,
-                       nullptr, stream);
+  return qf_stage_push(x, c_in, u_in, c0, c_out, u_out, aa, bb, t, dt, t_dev, toff, e0, n,
+                       x ? x->halo_ht : nullptr, nullptr, nullptr, stream);
 }
 
 int qf_stage_push(qf_ctx* x, const double* c_in, const double* u_in, const double* c0,
                   double* c_out, double* u_out, double aa, double bb, double t, double dt,
-                  const double* t_dev, double toff, int32_t e0, int32_t n, const int32_t* push,
-                  const qf_peer* peers, void* stream) {
+                  const double* t_dev, double toff, int32_t e0, int32_t n, const double* ht_in,
+                  const int32_t* push, const qf_peer* peers, void* stream) {
   if (!x || !c_in || !u_in || !c_out || !u_out) return fail(QF_E_ARG, "null argument");
   DevGuard guard(x);
   if (push && !peers) return fail(QF_E_ARG, "push table without peer table");
@@ -2152,6 +2225,7 @@ int qf_stage_push(qf_ctx* x, const double* c_in, const double* u_in, const doubl
   a.mode = 1;
   a.push = push;
   a.peers = peers;
+  a.ht = ht_in;
   QF_DISPATCH(x->d.order, launch_stage, x, a, (cudaStream_t)stream);
   return cuda_check("stage_kernel");
 }
@@ -2190,6 +2264,7 @@ static void step_impl(qf_ctx* x, double* c, double* u, double* work, double* t_d
     A.n = x->d.n_elem;
     A.terms = TERM_VOL | TERM_EDGE | TERM_SRC;
     A.mode = 1;
+    A.ht = x->halo_ht;
     const int si = A.gstage;
     if (2 * si + 1 < x->n_stage_ev) cudaEventRecordWithFlags(x->stage_ev[2 * si], s, cudaEventRecordExternal);
     QF_DISPATCH(k, launch_stage, x, A, s);
@@ -2269,6 +2344,21 @@ int qf_run(qf_ctx* x, int32_t n_steps, double* c, double* u, double* work, doubl
   }
   g_launches += (uint64_t)n_steps * kernels_per_step(x);
   return cuda_check("qf_run");
+}
+
+int qf_halo_table(qf_ctx* x, const double* ht) {
+  if (!x) return fail(QF_E_ARG, "null ctx");
+  x->halo_ht = ht;
+  return QF_OK;
+}
+
+int qf_halo_traces(qf_ctx* x, const double* c, const double* u, const int32_t* items, int32_t n,
+                   double* out, void* stream) {
+  if (!x || !c || !u || (n > 0 && (!items || !out))) return fail(QF_E_ARG, "null argument");
+  if (n <= 0) return QF_OK;
+  DevGuard guard(x);
+  QF_DISPATCH(x->d.order, launch_halo_traces, x, c, u, items, n, out, (cudaStream_t)stream);
+  return cuda_check("halo_trace_kernel");
 }
 
 int qf_user_scenario(qf_ctx* x, const void* image, size_t size, int32_t with_forcing) {
@@ -2433,6 +2523,14 @@ int qf_ipc_close_all(void) {
   for (auto& m : g_ipc_maps) cudaIpcCloseMemHandle(m.second);
   g_ipc_maps.clear();
   return cuda_check("cudaIpcCloseMemHandle");
+}
+
+int qf_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return QF_OK;
+  if (!dst || !src) return fail(QF_E_ARG, "null argument");
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess)
+    return cuda_check("qf_copy");
+  return QF_OK;
 }
 
 int qf_fill(double* buf, size_t n, double v, void* stream) {

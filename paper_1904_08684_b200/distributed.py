@@ -59,22 +59,41 @@ def range_partition(n_elem: int, world: int) -> np.ndarray:
 
 @dataclass
 class Halo:
-    """Local element order and exchange lists of one rank."""
+    """Local element order and halo-trace lists of one rank.
+
+    A rank stores only its owned elements (interior first, then
+    cut-adjacent).  For every cut edge (an edge whose other element belongs
+    to another rank) it keeps one row of a halo trace table: the other
+    element's trace moments of (xi, U, V, u, v, h_b) on that edge, 6 (k+1)
+    doubles, refreshed every stage by the owner.  Rows are
+    grouped by peer and, within a peer, ordered by global edge id, so both
+    sides of a cut enumerate it the same way."""
 
     rank: int
-    elements: np.ndarray          # global ids: owned (interior, then cut-adjacent), halo
+    elements: np.ndarray          # owned global ids: interior, then cut-adjacent
     n_own: int
     n_int: int                    # owned elements without a remote neighbour
-    send: dict = field(default_factory=dict)   # peer -> local ids (owned), peer's halo order
-    recv: dict = field(default_factory=dict)   # peer -> local ids (halo)
+    send: dict = field(default_factory=dict)   # peer -> (n, 2) [local slot, local edge], peer-row order
+    recv: dict = field(default_factory=dict)   # peer -> (first row, n rows) of my trace table
+    ht_code: np.ndarray = None    # (3, n_own): my trace-table row per (local edge, slot), -1 = none
 
     @property
     def n_local(self) -> int:
         return len(self.elements)
 
+    @property
+    def n_ht(self) -> int:
+        return sum(n for _, n in self.recv.values())
+
+    def items(self, p) -> np.ndarray:
+        """qf_halo_traces items (slot << 2 | local edge) of my send list to p."""
+        sl = self.send[p]
+        return (sl[:, 0] * 4 + sl[:, 1]).astype(np.int32)
+
 
 def build_halo(mesh: Mesh, part: np.ndarray, rank: int) -> Halo:
-    nbr = mesh.conn.nbr
+    cn = mesh.conn
+    nbr = cn.nbr
     own = np.flatnonzero(part == rank)
     nb = nbr[own]
     remote = (nb >= 0) & (part[np.maximum(nb, 0)] != rank)
@@ -84,22 +103,30 @@ def build_halo(mesh: Mesh, part: np.ndarray, rank: int) -> Halo:
     oi, ob = own[~cut], own[cut]
     own_order = np.concatenate([oi[locality_order(mesh, oi)], ob[locality_order(mesh, ob)]])
     n_own, n_int = len(own), int((~cut).sum())
-    rem = np.unique(nb[remote])
-    owner = part[rem]
-    order = np.lexsort((rem, owner))
-    halo = rem[order]
-    elements = np.concatenate([own_order, halo])
-    g2l = {int(g): i for i, g in enumerate(elements)}
-    recv, send = {}, {}
-    for p in np.unique(owner):
-        hp = halo[owner[order] == p]
-        recv[int(p)] = np.array([g2l[int(g)] for g in hp], dtype=np.int64)
-        # my owned elements adjacent to p, in global-id order (= p's halo order)
-        nbp = nbr[own_order]
-        mine = own_order[((nbp >= 0) & (part[np.maximum(nbp, 0)] == p)).any(axis=1)]
-        mine = np.sort(mine)
-        send[int(p)] = np.array([g2l[int(g)] for g in mine], dtype=np.int64)
-    return Halo(rank=rank, elements=elements, n_own=n_own, n_int=n_int, send=send, recv=recv)
+    g2l = np.full(mesh.n_triangles, -1, dtype=np.int64)
+    g2l[own_order] = np.arange(n_own)
+    # cut edges: (my global element, my local edge, peer, global edge id)
+    e_loc, j_loc = np.nonzero(remote)
+    ge = own[e_loc]
+    peer = part[nbr[ge, j_loc]]
+    eid = cn.elem_edge[ge, j_loc]
+    order = np.lexsort((eid, peer))
+    ge, j_loc, peer = ge[order], j_loc[order], peer[order]
+    ht_code = np.full((3, n_own), -1, dtype=np.int64)
+    send, recv = {}, {}
+    row = 0
+    for p in np.unique(peer):
+        sel = peer == p
+        n = int(sel.sum())
+        slots = g2l[ge[sel]]
+        # my rows for p's elements on these edges; the same edges, same order,
+        # are p's send list to me
+        ht_code[j_loc[sel], slots] = row + np.arange(n)
+        recv[int(p)] = (row, n)
+        send[int(p)] = np.column_stack([slots, j_loc[sel]]).astype(np.int64)
+        row += n
+    return Halo(rank=rank, elements=own_order, n_own=n_own, n_int=n_int, send=send, recv=recv,
+                ht_code=ht_code)
 
 
 PUSH_SLOT_BITS = 26
@@ -107,106 +134,89 @@ PUSH_SLOT_BITS = 26
 
 def push_table(halo: Halo, peer_recv: dict, ld: int) -> np.ndarray:
     """Destinations of the fused halo push (``qf_stage_push``): int32 [3][ld],
-    entry (peer << 26) | slot in the peer's local order, -1 = none.
-
-    ``peer_recv[p]`` is peer p's ``halo.recv[my rank]``: its halo slots of my
-    elements, in the same (global-id) order as my ``halo.send[p]``.  An
-    element adjacent to several peers gets one entry per peer (at most 3:
-    one per edge)."""
+    entry (peer << 26) | row of the peer's halo trace table for (local edge,
+    element), -1 = none.  ``peer_recv[p]`` is peer p's ``halo.recv[my rank]``
+    (first row, count); my ``send[p]`` lists the same cut edges in the same
+    order."""
     tab = np.full((3, ld), -1, dtype=np.int32)
-    fill = np.zeros(ld, dtype=np.int64)
-    for p, mine in halo.send.items():
-        dst = np.asarray(peer_recv[p], dtype=np.int64)
-        if len(dst) != len(mine):
+    for p, sl in halo.send.items():
+        first, n = peer_recv[p]
+        if n != len(sl):
             raise ValueError(f"halo lists of rank {halo.rank} and peer {p} disagree")
-        if p >= 1 << (31 - PUSH_SLOT_BITS) or (len(dst) and dst.max() >= 1 << PUSH_SLOT_BITS):
-            raise ValueError("push table overflow (peer or slot index)")
-        for e, d in zip(np.asarray(mine, dtype=np.int64), dst):
-            tab[fill[e], e] = (p << PUSH_SLOT_BITS) | int(d)
-            fill[e] += 1
+        if p >= 1 << (31 - PUSH_SLOT_BITS) or first + n > 1 << PUSH_SLOT_BITS:
+            raise ValueError("push table overflow (peer or row index)")
+        if (tab[sl[:, 1], sl[:, 0]] != -1).any():
+            raise ValueError("a cut edge has two peers")
+        tab[sl[:, 1], sl[:, 0]] = (p << PUSH_SLOT_BITS) | (first + np.arange(n))
     return tab
 
 
 def peer_table(torch, entries, device):
-    """Device qf_peer[] table: entries[p] = (c_ptr, u_ptr, ld) or None."""
-    t = torch.zeros((max(len(entries), 1), 3), dtype=torch.int64)
+    """Device qf_peer[] table: entries[p] = halo trace table pointer of peer p, or None."""
+    t = torch.zeros((max(len(entries), 1), 1), dtype=torch.int64)
     for p, ent in enumerate(entries):
         if ent is not None:
-            t[p, 0], t[p, 1], t[p, 2] = int(ent[0]), int(ent[1]), int(ent[2])
+            t[p, 0] = int(ent)
     return t.to(device)
 
 
 # ----------------------------------------------------------------- exchange
 class HaloExchange:
-    """Pack (c, u) rows of the send lists, P2P exchange, unpack into the halo.
+    """Halo trace rows of the send lists -> P2P exchange -> row ranges of the
+    peers' halo trace tables.
 
-    ``c``/``u`` are [F][K][ld] tensors (device for NCCL, CPU for gloo).  On
-    the GPU, gather/scatter are the library kernels; the transfers are
-    ``torch.distributed.batch_isend_irecv`` (NCCL P2P over NVLink).
+    On the GPU the rows are computed by ``qf_halo_traces`` (the stage
+    kernel's rounding) and moved by ``torch.distributed.batch_isend_irecv``
+    (NCCL P2P over NVLink) straight into the receiving table; on the CPU
+    (``gloo`` tests) ``tracer(c, u, items) -> (n, 6, NT)`` computes them.
     """
 
-    def __init__(self, halo: Halo, K: int, ld: int, device, lib=None):
+    def __init__(self, halo: Halo, NT: int, device, lib=None, ctx=None, tracer=None):
         import torch
 
         self.torch = torch
-        self.halo, self.K, self.ld, self.lib = halo, K, ld, lib
-        self.rows = 5 * K
+        self.halo, self.W, self.lib, self.ctx, self.tracer = halo, 6 * NT, lib, ctx, tracer
         self.dev = device
         self.peers = sorted(set(halo.send) | set(halo.recv))
-        self.sidx = {p: torch.as_tensor(halo.send.get(p, np.zeros(0, np.int64)).astype(np.int32),
-                                        device=device) for p in self.peers}
-        self.ridx = {p: torch.as_tensor(halo.recv.get(p, np.zeros(0, np.int64)).astype(np.int32),
-                                        device=device) for p in self.peers}
-        self.sbuf = {p: torch.empty(self.rows * len(self.sidx[p]), dtype=torch.float64,
-                                    device=device) for p in self.peers}
-        self.rbuf = {p: torch.empty(self.rows * len(self.ridx[p]), dtype=torch.float64,
-                                    device=device) for p in self.peers}
+        self.items = {p: torch.as_tensor(halo.items(p), device=device) for p in halo.send}
+        self.sbuf = {p: torch.empty(len(self.items[p]) * self.W, dtype=torch.float64,
+                                    device=device) for p in halo.send}
 
-    def _gather(self, c, u, p, stream):
-        n = len(self.sidx[p])
+    def traces(self, c, u, p, stream=None):
+        """My rows for peer p (its trace-table rows for our cut edges)."""
+        n = len(self.items[p])
         buf = self.sbuf[p]
         if self.lib is not None:
-            s = stream.cuda_stream
-            self.lib.qf_gather(c.data_ptr(), self.ld, self.sidx[p].data_ptr(), n, 3 * self.K,
-                               buf.data_ptr(), s)
-            self.lib.qf_gather(u.data_ptr(), self.ld, self.sidx[p].data_ptr(), n, 2 * self.K,
-                               buf[3 * self.K * n:].data_ptr(), s)
-        else:
-            idx = self.sidx[p].long()
-            buf.view(self.rows, n)[: 3 * self.K] = c.view(3 * self.K, self.ld)[:, idx]
-            buf.view(self.rows, n)[3 * self.K:] = u.view(2 * self.K, self.ld)[:, idx]
+            s = stream.cuda_stream if stream is not None else \
+                self.torch.cuda.current_stream().cuda_stream
+            from . import _cabi
+            _cabi.check(self.lib.qf_halo_traces(self.ctx, c.data_ptr(), u.data_ptr(),
+                                                self.items[p].data_ptr(), n, buf.data_ptr(), s),
+                        "qf_halo_traces")
+        elif n:
+            npy = lambda a: a.numpy() if hasattr(a, "numpy") else a  # noqa: E731
+            rows = self.tracer(npy(c), npy(u), self.items[p].numpy())
+            buf.copy_(self.torch.as_tensor(np.ascontiguousarray(rows)).reshape(-1))
+        return buf
 
-    def _scatter(self, c, u, p, stream):
-        n = len(self.ridx[p])
-        buf = self.rbuf[p]
-        if self.lib is not None:
-            s = stream.cuda_stream
-            self.lib.qf_scatter(buf.data_ptr(), self.ridx[p].data_ptr(), n, 3 * self.K,
-                                c.data_ptr(), self.ld, s)
-            self.lib.qf_scatter(buf[3 * self.K * n:].data_ptr(), self.ridx[p].data_ptr(), n,
-                                2 * self.K, u.data_ptr(), self.ld, s)
-        else:
-            idx = self.ridx[p].long()
-            c.view(3 * self.K, self.ld)[:, idx] = buf.view(self.rows, n)[: 3 * self.K]
-            u.view(2 * self.K, self.ld)[:, idx] = buf.view(self.rows, n)[3 * self.K:]
-
-    def exchange(self, c, u, stream=None):
-        """Blocking (w.r.t. ``stream``) halo update of (c, u)."""
+    def exchange(self, c, u, ht, stream=None):
+        """Blocking (w.r.t. ``stream``) refresh of the halo trace table ``ht``
+        ((n_ht, 6 NT) tensor) from the peers' (c, u)."""
         import torch.distributed as dist
 
-        for p in self.peers:
-            self._gather(c, u, p, stream)
+        for p in self.halo.send:
+            self.traces(c, u, p, stream)
         ops = []
+        flat = ht.view(-1)
         for p in self.peers:
-            if len(self.sbuf[p]):
+            if p in self.sbuf and len(self.sbuf[p]):
                 ops.append(dist.P2POp(dist.isend, self.sbuf[p], p))
-            if len(self.rbuf[p]):
-                ops.append(dist.P2POp(dist.irecv, self.rbuf[p], p))
+            if p in self.halo.recv and self.halo.recv[p][1]:
+                first, n = self.halo.recv[p]
+                ops.append(dist.P2POp(dist.irecv, flat[first * self.W:(first + n) * self.W], p))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        for p in self.peers:
-            self._scatter(c, u, p, stream)
 
 
 def rk_plan(k: int):
@@ -220,7 +230,7 @@ def rk_plan(k: int):
 
 # ------------------------------------------------------------- GPU runner
 class PartitionRunner:
-    """Device state and stage launches of one partition (owned + halo)."""
+    """Device state, halo trace tables and stage launches of one partition."""
 
     def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int):
         import torch
@@ -231,25 +241,44 @@ class PartitionRunner:
         self.k = order
         self.halo = build_halo(mesh, part, rank)
         h = self.halo
-        self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own)
+        self.disc = Discretization(mesh, scenario, order, elements=h.elements, n_own=h.n_own,
+                                   halo_code=h.ht_code)
         d = self.disc
         self.K, self.ld, self.lib = d.K, d.ld, d._lib
+        self.NT = order + 1
         self.c = d._c_init.clone() if d.device_setup else d.upload_fields(d.project_fields())
         self.u = torch.zeros_like(self.c[:2])
         self.bufs = {0: (self.c, self.u),
                      1: (torch.zeros_like(self.c), torch.zeros_like(self.u)),
                      2: (torch.zeros_like(self.c), torch.zeros_like(self.u))}
+        # halo trace table per RK buffer: rows for the stage reading that buffer
+        self.ht = {b: torch.zeros((max(h.n_ht, 1), 6 * self.NT), dtype=torch.float64,
+                                  device=d.device) for b in range(3)}
         s = torch.cuda.current_stream().cuda_stream
-        # halo velocities are element-local: solve them locally at start
         d._check(self.lib.qf_velocity(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0,
-                                      h.n_local, s), "qf_velocity")
+                                      h.n_own, s), "qf_velocity")
         self.dt = d.dt
         self.t = 0.0
+
+    def traces_for(self, p, b=0, out=None):
+        """My halo trace rows for peer p from RK buffer b (device tensor)."""
+        torch, h = self.torch, self.halo
+        items = torch.as_tensor(h.items(p), device=self.disc.device)
+        n = len(items)
+        out = torch.empty((max(n, 1), 6 * self.NT), dtype=torch.float64,
+                          device=self.disc.device) if out is None else out
+        c, u = self.bufs[b]
+        self.disc._check(self.lib.qf_halo_traces(self.disc._ctx, c.data_ptr(), u.data_ptr(),
+                                                 items.data_ptr(), n, out.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream),
+                         "qf_halo_traces")
+        return out[:n]
 
     def local_lambda_max(self) -> float:
         d, torch = self.disc, self.torch
         lam = torch.zeros((3, self.ld), dtype=torch.float64, device=d.device)
         out = torch.empty_like(self.c)
+        d._check(self.lib.qf_halo_table(d._ctx, self.ht[0].data_ptr()), "qf_halo_table")
         d._check(self.lib.qf_rhs(d._ctx, self.c.data_ptr(), self.u.data_ptr(), 0.0, 2,
                                  out.data_ptr(), lam.data_ptr(),
                                  torch.cuda.current_stream().cuda_stream), "qf_rhs")
@@ -264,8 +293,9 @@ class PartitionRunner:
     def stage(self, si: int, part: str, stream, ghost: bool = True, push=None, peers=None):
         """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range
         (with ``ghost``, the interior / all launch is preceded by the stage's
-        Dirichlet data).  ``push``/``peers`` (device tensors): fused halo push
-        of the new cut-adjacent rows into the peers' stage-output buffers."""
+        Dirichlet data).  Halo neighbours are read from the trace table of the
+        stage input; ``push``/``peers`` (device tensors): fused push of the
+        new cut-edge traces into the peers' tables for the stage output."""
         src, dst, a, b, toff = rk_plan(self.k)[si]
         d, lib, h = self.disc, self.lib, self.halo
         s = stream.cuda_stream
@@ -276,15 +306,13 @@ class PartitionRunner:
         co, uo = self.bufs[dst]
         e0, n = {"interior": (0, h.n_int), "boundary": (h.n_int, h.n_own - h.n_int),
                  "all": (0, h.n_own)}[part]
-        if n > 0 and push is not None:
+        if n > 0:
             d._check(lib.qf_stage_push(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
                                        co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None,
-                                       0.0, e0, n, push.data_ptr(), peers.data_ptr(), s),
+                                       0.0, e0, n, self.ht[src].data_ptr(),
+                                       None if push is None else push.data_ptr(),
+                                       None if peers is None else peers.data_ptr(), s),
                      "qf_stage_push")
-        elif n > 0:
-            d._check(lib.qf_stage(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
-                                  co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None, 0.0, e0,
-                                  n, s), "qf_stage")
         return co, uo
 
     def end_step(self):
@@ -293,6 +321,7 @@ class PartitionRunner:
                                                          or self.torch.cuda.current_stream())
             self.c.copy_(self.bufs[1][0])
             self.u.copy_(self.bufs[1][1])
+            self.ht[0].copy_(self.ht[1])
         self.t += self.dt
 
 
@@ -319,7 +348,13 @@ class DistributedRunner(PartitionRunner):
             # these GPUs); recorded in the bench line
             self.transport = "nccl"
         if self.transport == "nccl":
-            self.ex = HaloExchange(self.halo, self.K, self.ld, self.disc.device, lib=self.lib)
+            # initial halo traces (state of buffer 0); repeated after every stage
+            self.ex = HaloExchange(self.halo, self.NT, self.disc.device, lib=self.lib,
+                                   ctx=self.disc._ctx)
+            self.ex.exchange(self.c, self.u, self.ht[0])
+            torch.cuda.synchronize()
+        else:
+            self._initial_push()
         if scenario.cfl is not None:
             lmax = torch.tensor([self.local_lambda_max()], dtype=torch.float64, device="cuda")
             hmin = torch.tensor([self.disc.h_min], dtype=torch.float64, device="cuda")
@@ -331,9 +366,9 @@ class DistributedRunner(PartitionRunner):
         self.bnd = torch.cuda.Stream()
 
     def _setup_p2p(self, mesh, part) -> bool:
-        """Fused transport: map the peers' stage buffers (CUDA IPC over
+        """Fused transport: map the peers' halo trace tables (CUDA IPC over
         NVLink) and build the push table; per stage the cut-adjacent launch
-        stores its new rows straight into the peers' halo slots and raises a
+        stores its new cut-edge traces straight into the peers' tables and raises a
         per-peer flag (stream memory operation); the peer's next cut-adjacent
         launch waits on that flag (no NCCL, no gather / scatter kernels).
         Collective-safe: every rank reaches the same collectives and all
@@ -344,7 +379,7 @@ class DistributedRunner(PartitionRunner):
         h = self.halo
         self.peers = sorted(set(h.send) | set(h.recv))
         self.flags = torch.zeros(self.world, dtype=torch.int32, device=self.disc.device)
-        bufs = [t for b in range(3) for t in self.bufs[b]] + [self.flags]
+        bufs = [self.ht[b] for b in range(3)] + [self.flags]
         mine, err = [], None
         try:
             for t in bufs:
@@ -356,9 +391,8 @@ class DistributedRunner(PartitionRunner):
         except Exception as exc:  # noqa: BLE001 (reported, all ranks fall back)
             err, mine = exc, None
         info = [None] * self.world
-        dist.all_gather_object(info, {"ipc": mine, "recv": {int(p): v.tolist()
-                                                            for p, v in h.recv.items()},
-                                      "ld": self.ld})
+        dist.all_gather_object(info, {"ipc": mine, "recv": {int(p): list(v)
+                                                            for p, v in h.recv.items()}})
         try:
             if err is not None:
                 raise err
@@ -375,12 +409,13 @@ class DistributedRunner(PartitionRunner):
             dev = self.disc.device
             self.push = torch.as_tensor(push_table(h, {p: info[p]["recv"][self.rank]
                                                        for p in h.send}, self.ld), device=dev)
-            self.peer_bufs = [peer_table(torch, [(ptrs[p][2 * b], ptrs[p][2 * b + 1],
-                                                  info[p]["ld"]) if p in ptrs else None
+            self.peer_ht = ptrs
+            self.peer_recv = {p: info[p]["recv"][self.rank] for p in h.send}
+            self.peer_bufs = [peer_table(torch, [ptrs[p][b] if p in ptrs else None
                                                  for p in range(self.world)], dev)
                               for b in range(3)]
             # my flag slot in each peer's flag array; handshake write of 0
-            self.remote_flag = {p: ptrs[p][6] + 4 * self.rank for p in self.peers}
+            self.remote_flag = {p: ptrs[p][3] + 4 * self.rank for p in self.peers}
             s = torch.cuda.current_stream().cuda_stream
             for p in self.peers:
                 self.disc._check(lib.qf_signal(self.remote_flag[p], 0, s), "qf_signal")
@@ -399,6 +434,22 @@ class DistributedRunner(PartitionRunner):
             return False
         self.gen = 0  # stages completed (flag value)
         return True
+
+    def _initial_push(self):
+        """Initial halo traces over the mapped peer tables: my rows for each
+        peer copied into its table 0, then a barrier (no rank steps before
+        every table holds the initial state's traces)."""
+        torch, lib = self.torch, self.lib
+        W = 6 * self.NT
+        s = torch.cuda.current_stream().cuda_stream
+        for p in self.halo.send:
+            rows = self.traces_for(p, 0)
+            first, n = self.peer_recv[p]
+            if n:
+                self.disc._check(lib.qf_copy(self.peer_ht[p][0] + 8 * first * W, rows.data_ptr(),
+                                             8 * n * W, s), "qf_copy")
+        torch.cuda.synchronize()
+        self.dist.barrier()
 
     def _step_p2p(self):
         torch, lib = self.torch, self.lib
@@ -446,7 +497,7 @@ class DistributedRunner(PartitionRunner):
             co, uo = self.stage(si, "boundary", self.bnd, ghost=False)
             self.comm.wait_stream(self.bnd)
             with torch.cuda.stream(self.comm):
-                self.ex.exchange(co, uo, self.comm)
+                self.ex.exchange(co, uo, self.ht[rk_plan(self.k)[si][1]], self.comm)
             main.wait_stream(self.bnd)               # next stage's interior reads these rows
         self.end_step()
 
@@ -458,9 +509,11 @@ class DistributedRunner(PartitionRunner):
 
 
 class LocalMultiRunner:
-    """All partitions in one process on one GPU, halos moved by device
-    gather/scatter between the partitions' buffers (fake transport for
-    single-GPU tests of the partitioned kernels)."""
+    """All partitions in one process on one GPU (single-GPU tests of the
+    partitioned kernels): the halo trace rows are either
+    pushed by the stage kernels into each other's tables (``push``, the
+    fused transport) or computed by ``qf_halo_traces`` from the peer's
+    stage output and copied (``gather``, what the NCCL transport moves)."""
 
     def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray,
                  transport: str = "gather"):
@@ -471,44 +524,32 @@ class LocalMultiRunner:
         self.parts = [PartitionRunner(mesh, scenario, order, part, r) for r in range(world)]
         self.k = order
         self.transport = transport
-        if transport == "push":  # fused: stage kernels store into each other's halo slots
+        if transport == "push":
             for r, pr in enumerate(self.parts):
                 recv = {p: self.parts[p].halo.recv[r] for p in pr.halo.send}
                 pr.push_tab = torch.as_tensor(push_table(pr.halo, recv, pr.ld), device="cuda")
-                pr.peer_bufs = [peer_table(torch, [(q.bufs[b][0].data_ptr(), q.bufs[b][1].data_ptr(),
-                                                    q.ld) for q in self.parts], "cuda")
+                pr.peer_bufs = [peer_table(torch, [q.ht[b].data_ptr() for q in self.parts], "cuda")
                                 for b in range(3)]
-        idx = lambda a: torch.as_tensor(a.astype(np.int32), device="cuda")  # noqa: E731
-        self.links = []
+        self._refresh(0)  # halo traces of the initial state
+
+    def _refresh(self, b):
+        """Every partition's table b from its peers' buffer b."""
         for r, pr in enumerate(self.parts):
-            for p, recv in pr.halo.recv.items():
-                send = self.parts[p].halo.send[r]
-                self.links.append((r, p, idx(recv), idx(send)))
+            for p, (first, n) in pr.halo.recv.items():
+                if n:
+                    pr.ht[b][first:first + n].copy_(self.parts[p].traces_for(r, b))
 
     def step(self):
-        torch = self.torch
-        s = torch.cuda.current_stream()
-        if self.transport == "push":
-            for si in range(len(rk_plan(self.k))):
-                dst = rk_plan(self.k)[si][1]
-                for pr in self.parts:
-                    pr.stage(si, "all", s, push=pr.push_tab, peers=pr.peer_bufs[dst])
-            for pr in self.parts:
-                pr.end_step()
-            return
+        s = self.torch.cuda.current_stream()
         for si in range(len(rk_plan(self.k))):
-            outs = [pr.stage(si, "all", s) for pr in self.parts]
-            for r, p, ridx, sidx in self.links:
-                dst, src = self.parts[r], self.parts[p]
-                n = len(ridx)
-                tmp = torch.empty(5 * dst.K * n, dtype=torch.float64, device="cuda")
-                for f, (arr_src, arr_dst, rows) in enumerate(
-                        ((outs[p][0], outs[r][0], 3 * dst.K), (outs[p][1], outs[r][1], 2 * dst.K))):
-                    off = 0 if f == 0 else 3 * dst.K * n
-                    src.lib.qf_gather(arr_src.data_ptr(), src.ld, sidx.data_ptr(), n, rows,
-                                      tmp[off:].data_ptr(), s.cuda_stream)
-                    dst.lib.qf_scatter(tmp[off:].data_ptr(), ridx.data_ptr(), n, rows,
-                                       arr_dst.data_ptr(), dst.ld, s.cuda_stream)
+            dst = rk_plan(self.k)[si][1]
+            for pr in self.parts:
+                if self.transport == "push":
+                    pr.stage(si, "all", s, push=pr.push_tab, peers=pr.peer_bufs[dst])
+                else:
+                    pr.stage(si, "all", s)
+            if self.transport != "push":
+                self._refresh(dst)
         for pr in self.parts:
             pr.end_step()
 

@@ -9,16 +9,17 @@ per (field, mode):
     geo       [6][ld]      B11, B12, B21, B22, a1x, a1y
     hb        [NH][ld]     projected bathymetry coefficients (NH = 1 or 3)
     nbr       [3][ld]      int32 neighbour code per local edge:
-                             >= 0 : 4 * neighbour + neighbour's local edge
+                             >= 0 : 4 * neighbour + neighbour's local edge,
+                                    or 4 * h + 3: row h of the halo trace
+                                    table (partitions, distributed.py)
                              <  0 : boundary, -1 - (2 * slot + kind),
                                     kind 0 = Dirichlet (slot indexes the
                                     per-stage ghost table), 1 = wall
     bnd       [nb]         (element, local edge) of each Dirichlet slot
 
 ``ld`` = element count rounded up to a multiple of 32 (alignment of every
-row to 256 B).  Elements [E, ld) are padding and never touched; with a halo
-(multi-GPU partitions) owned elements come first and halo copies of
-neighbour-rank elements follow, see ``distributed.py``.
+row to 256 B).  Elements [E, ld) are padding and never touched; a
+partition holds only its owned elements (see ``distributed.py``).
 """
 
 from __future__ import annotations
@@ -32,6 +33,7 @@ from .mesh import Mesh, compute_geometry
 __all__ = ["ElementTables", "build_tables", "pad_ld", "aos_to_soa", "soa_to_aos"]
 
 BND_DIRICHLET, BND_WALL = 0, 1
+HALO_J = 3  # neighbour code 4 h + 3: row h of the halo trace table (csrc HALO_J)
 
 
 def pad_ld(n: int) -> int:
@@ -50,15 +52,15 @@ class ElementTables:
     h_min: float
 
 
-def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, elements=None, n_own=None
-                 ) -> ElementTables:
+def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, elements=None, n_own=None,
+                 halo_code=None) -> ElementTables:
     """Geometry and neighbour codes.
 
     ``elements`` (global ids, local order) restricts the tables to a
-    partition: the first ``n_own`` are updated by this context, the rest are
-    halo copies of neighbour-rank elements (geometry / bathymetry only, their
-    state arrives by exchange).  Every neighbour of an owned element must be
-    in ``elements``.
+    partition: the first ``n_own`` are updated by this context.  A neighbour
+    outside ``elements`` is another partition's element whose edge traces
+    arrive in row h = ``halo_code[j][slot]`` of the halo trace table: code
+    4 h + 3 (``HALO_J``).
     """
     geom, egeom = compute_geometry(mesh)
     c = mesh.conn
@@ -79,10 +81,18 @@ def build_tables(mesh: Mesh, dirichlet_markers, wall_markers, elements=None, n_o
     nbr, nloc = c.nbr[own], c.nbr_local[own]
     inner = nbr >= 0
     lnb = np.where(inner, g2l[np.maximum(nbr, 0)], 0)
-    if (lnb[inner] < 0).any():
-        raise ValueError("partition is missing halo elements")
     code = np.zeros((3, ld), dtype=np.int64)
     code[:, :E] = np.where(inner, 4 * lnb + np.maximum(nloc, 0), 0).T
+    ext = inner & (lnb < 0)  # neighbour owned by another partition
+    if ext.any():
+        if halo_code is None:
+            raise ValueError("partition has remote neighbours but no halo trace rows")
+        hc = np.asarray(halo_code)[:, :E].T  # (E, 3)
+        if (hc[ext] < 0).any():
+            raise ValueError("a remote neighbour has no halo trace row")
+        ce = code[:, :E].T.copy()
+        ce[ext] = 4 * hc[ext] + HALO_J
+        code[:, :E] = ce.T
     bel, bj = np.nonzero(~inner)
     marks = -nloc[bel, bj]
     dmask = np.isin(marks, list(dirichlet_markers))

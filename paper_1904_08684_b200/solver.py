@@ -162,9 +162,11 @@ class HostSetup:
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
                  elements=None, n_own: int | None = None, device_setup: bool | None = None,
-                 slot_order: str = "locality"):
+                 slot_order: str = "locality", halo_code=None):
         """``elements``/``n_own`` restrict the discretization to a partition
-        (``distributed.py``): local order = owned elements then halo copies.
+        (``distributed.py``): the owned elements, interior first; neighbours
+        owned by other partitions are rows of a halo trace table
+        (``halo_code[j][slot]``, see ``distributed.Halo``).
         ``device_setup`` moves the initial / bathymetry projections to the GPU
         (``qf_project``; default: automatic for large meshes).  ``slot_order``:
         device element slots in Z-order ("locality", default) or mesh order
@@ -215,7 +217,7 @@ class HostSetup:
             self.perm = locality_order(mesh)
         slots = self.elements if self.perm is None else self.elements[self.perm]
         self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
-                                   slots, self.n_own)
+                                   slots, self.n_own, halo_code=halo_code)
         self.h_min = self.tables.h_min
         if not scenario.device_matches():
             raise ValueError(f"scenario {scenario.name!r}: hb / exact / forcing / mass_source / g / "
@@ -309,8 +311,9 @@ class Discretization(HostSetup):
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
                  device: int | None = None, elements=None, n_own: int | None = None,
-                 device_setup: bool | None = None, slot_order: str = "locality"):
-        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup, slot_order)
+                 device_setup: bool | None = None, slot_order: str = "locality", halo_code=None):
+        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup, slot_order,
+                         halo_code)
         self._setup_device(device)
 
     def _setup_device(self, device):

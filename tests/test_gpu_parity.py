@@ -133,9 +133,10 @@ def test_p4_mms_vs_oracle():
                                          (1, "mms", "ranges"), (4, "walls", "blocks")])
 def test_partitioned_gpu_equals_single_domain(k, case, part, transport):
     """Partitioned stage kernels reproduce the single-domain GPU run bit for
-    bit, with the halo moved by device gather/scatter or by the fused push
-    (qf_stage_push: the stage / velocity kernel stores the new cut-adjacent
-    rows straight into the other partitions' halo slots)."""
+    bit, with the halo trace rows computed by qf_halo_traces and copied
+    (what the NCCL transport moves) or pushed by the fused transport
+    (qf_stage_push: the stage / velocity kernel stores the new cut-edge
+    traces straight into the other partitions' halo trace tables)."""
     from paper_1904_08684_b200 import distributed as D, mesh as M, scenario as S
     n, steps = 16, 4
     mesh = M.build_unit_square_mesh(n)
@@ -345,7 +346,8 @@ def test_l2_error_device_matches_host(k, n, steps):
     tot = np.zeros(3)
     for r in range(2):
         h = build_halo(mesh, part, r)
-        d = Discretization(mesh, scn, k, elements=h.elements, n_own=h.n_own)
+        d = Discretization(mesh, scn, k, elements=h.elements, n_own=h.n_own,
+                           halo_code=h.ht_code)
         c = st.c[h.elements]
         from paper_1904_08684_b200.solver import DeviceState
         cd = d.upload_fields(c)
