@@ -287,7 +287,7 @@ class PartitionRunner:
     def ghost(self, si: int, stream):
         """Dirichlet data of stage ``si`` (read by both ranges of the stage)."""
         d = self.disc
-        if d.tables.bnd_elem.size:
+        if int(d.tables.bnd_elem.shape[0]):
             self.lib.qf_ghost(d._ctx, self.t + rk_plan(self.k)[si][4] * self.dt, stream.cuda_stream)
 
     def stage(self, si: int, part: str, stream, ghost: bool = True, push=None, peers=None):

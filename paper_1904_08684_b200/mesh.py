@@ -107,8 +107,15 @@ class Mesh:
     vertices: np.ndarray      # (NV, 2) float64
     triangles: np.ndarray     # (E, 3) int64, counter-clockwise
     boundary_markers: dict = field(default_factory=dict)
-    conn: Connectivity | None = None
+    _conn: Connectivity | None = field(default=None, repr=False)
     _edges_cache: list | None = field(default=None, repr=False)
+
+    @property
+    def conn(self) -> Connectivity:
+        """Flat connectivity tables (built on first use for lazily built meshes)."""
+        if self._conn is None:
+            build_connectivity(self)
+        return self._conn
 
     @property
     def n_vertices(self) -> int:
@@ -185,7 +192,7 @@ def build_connectivity(mesh: Mesh) -> None:
     nbr_local[left[it], left_local[it]] = right_local[it]
     nbr[right[it], right_local[it]] = left[it]
     nbr_local[right[it], right_local[it]] = left_local[it]
-    mesh.conn = Connectivity(
+    mesh._conn = Connectivity(
         v0=u[first], v1=v[first], left=left, left_local=left_local, right=right,
         right_local=right_local, marker=marker, elem_edge=elem_edge, nbr=nbr,
         nbr_local=nbr_local)
@@ -216,9 +223,10 @@ def jitter_unit(seed: int, vertex_ids: np.ndarray, coord: int, retry) -> np.ndar
     return _splitmix64(key).astype(np.float64) / 2.0**63 - 1.0
 
 
-def _finish(vertices, triangles, markers=None) -> Mesh:
+def _finish(vertices, triangles, markers=None, lazy: bool = False) -> Mesh:
     mesh = Mesh(vertices=vertices, triangles=triangles, boundary_markers=markers or {})
-    build_connectivity(mesh)
+    if not lazy:
+        build_connectivity(mesh)
     return mesh
 
 
@@ -259,13 +267,15 @@ def build_square_mesh(level: int, perturb: float = 0.0, seed: int = 0) -> Mesh:
 
 
 def build_unit_square_mesh(n: int, jitter: float = 0.0, seed: int = 0,
-                           length: float = 1.0) -> Mesh:
+                           length: float = 1.0, lazy: bool = False) -> Mesh:
     """BASELINE mesh: [0,L]^2, n x n quads, every quad split SW-NE into
     (v00, v10, v11), (v00, v11, v01); vertex id = i*(n+1)+j (x index i).
 
     ``jitter`` > 0 displaces INTERIOR vertices by jitter*h*u, u in [-1, 1)
     from ``jitter_unit`` (SplitMix64 keyed by seed/vertex/coord, retry 0).
     With jitter <= 0.25 no triangle can invert (min altitude h/sqrt2).
+    ``lazy``: connectivity is built on first use of ``mesh.conn`` (the device
+    setup path, device_setup.py, never needs it).
     """
     if n < 1:
         raise ValueError("n must be >= 1")
@@ -289,7 +299,7 @@ def build_unit_square_mesh(n: int, jitter: float = 0.0, seed: int = 0,
             verts[inner, c] += jitter * h * jitter_unit(seed, ids, c, 0)
         if (_signed_dets(verts, tris) <= 0.0).any():
             raise DegenerateElement("jitter inverted a triangle")
-    return _finish(verts, tris)
+    return _finish(verts, tris, lazy=lazy)
 
 
 def build_ring_mesh(level: int) -> Mesh:

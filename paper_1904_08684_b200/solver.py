@@ -162,7 +162,7 @@ class HostSetup:
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
                  elements=None, n_own: int | None = None, device_setup: bool | None = None,
-                 slot_order: str = "locality", halo_code=None):
+                 slot_order: str = "locality", halo_code=None, device_tables: bool | None = None):
         """``elements``/``n_own`` restrict the discretization to a partition
         (``distributed.py``): the owned elements, interior first; neighbours
         owned by other partitions are rows of a halo trace table
@@ -171,7 +171,11 @@ class HostSetup:
         (``qf_project``; default: automatic for large meshes).  ``slot_order``:
         device element slots in Z-order ("locality", default) or mesh order
         ("natural") or a seeded shuffle ("random", for tests: every neighbour out
-        of block); results are identical, only the memory locality differs."""
+        of block); results are identical, only the memory locality differs.
+        ``device_tables`` builds connectivity, geometry, Z-order slots and the
+        SoA tables on the GPU (``device_setup.py``; default: with
+        ``device_setup`` on a whole mesh); host geometry and connectivity are
+        then computed only if an API asks for them."""
         if slot_order not in ("locality", "natural", "random"):
             raise ValueError("slot_order must be 'locality', 'natural' or 'random'")
         self.slot_order = slot_order
@@ -185,46 +189,57 @@ class HostSetup:
         self.backend = backend  # accepted for signature compatibility only
         self.basis = build_basis(self.k)
         self.K = self.basis.size
-        geom, self.edge_geom = compute_geometry(mesh)
+        self._geom = self._edge_geom = None
         self.partitioned = elements is not None
         if elements is None:
             self.elements = np.arange(mesh.n_triangles)
             self.n_own = mesh.n_triangles
-            self.geom = geom
         else:
             self.elements = np.asarray(elements, dtype=np.int64)
             self.n_own = len(self.elements) if n_own is None else int(n_own)
-            el = self.elements
-            self.geom = ElementGeometry(B=geom.B[el], detB=geom.detB[el],
-                                        sqrt_detB=geom.sqrt_detB[el], a1=geom.a1[el])
         prog = scenario.field_program()
         if device_setup is None:
             device_setup = prog is not None and len(self.elements) >= self.DEVICE_SETUP_MIN
         if device_setup and prog is None:
             raise ValueError(f"scenario {scenario.name!r} has no device field program")
         self.device_setup = bool(device_setup)
+        if device_tables is None:
+            device_tables = self.device_setup and not self.partitioned and slot_order == "locality"
+        self.device_tables = bool(device_tables)
         self._nh = 1 if self.k == 0 else 3
         self._setup_quadrature()
         if not self.device_setup:
             self._setup_bathymetry()
-        # device slot order: locality (Z-order) permutation of the local rows
-        # for a whole mesh; a partition's local order is already sorted
-        if self.partitioned or self.slot_order == "natural":
-            self.perm = None
-        elif self.slot_order == "random":
-            self.perm = np.random.default_rng(0).permutation(mesh.n_triangles)
+        self._perm_host = None
+        if self.device_tables:
+            from .device_setup import device_tables as build_device_tables
+            import torch
+
+            if self.partitioned or slot_order != "locality":
+                raise ValueError("device tables are built for whole meshes in Z-order slots")
+            self.tables = build_device_tables(mesh, scenario.dirichlet_markers,
+                                              scenario.wall_markers,
+                                              torch.device("cuda", torch.cuda.current_device()))
+            self.setup_seconds = self.tables.seconds
         else:
-            self.perm = locality_order(mesh)
-        slots = self.elements if self.perm is None else self.elements[self.perm]
-        self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
-                                   slots, self.n_own, halo_code=halo_code)
+            # device slot order: locality (Z-order) permutation of the local rows
+            # for a whole mesh; a partition's local order is already sorted
+            if self.partitioned or self.slot_order == "natural":
+                self._perm_host = None
+            elif self.slot_order == "random":
+                self._perm_host = np.random.default_rng(0).permutation(mesh.n_triangles)
+            else:
+                self._perm_host = locality_order(mesh)
+            slots = self.elements if self._perm_host is None else self.elements[self._perm_host]
+            self.tables = build_tables(mesh, scenario.dirichlet_markers, scenario.wall_markers,
+                                       slots, self.n_own, halo_code=halo_code)
         self.h_min = self.tables.h_min
         if not scenario.device_matches():
             raise ValueError(f"scenario {scenario.name!r}: hb / exact / forcing / mass_source / g / "
                              "tau_bf / f_c were changed after its device family was built; the "
                              "kernels would evaluate different physics than the host callables "
                              "(build a new scenario instead)")
-        needs_data = len(self.tables.bnd_elem) > 0 or scenario.forcing is not None \
+        needs_data = int(self.tables.bnd_elem.shape[0]) > 0 or scenario.forcing is not None \
             or scenario.mass_source is not None
         if needs_data and scenario.device.kind == KIND_NONE:
             raise ValueError(f"scenario {scenario.name!r} needs boundary data or forcing that "
@@ -242,6 +257,34 @@ class HostSetup:
              for f in self.basis.functions])
 
     # ------------------------------------------------------------- setup
+    @property
+    def perm(self):
+        """Device slot -> local element row (None: identity); host copy."""
+        if self.device_tables and self._perm_host is None:
+            self._perm_host = self.tables.perm.cpu().numpy()
+        return self._perm_host
+
+    def _host_geometry(self):
+        geom, self._edge_geom = compute_geometry(self.mesh)
+        if self.partitioned:
+            el = self.elements
+            geom = ElementGeometry(B=geom.B[el], detB=geom.detB[el],
+                                   sqrt_detB=geom.sqrt_detB[el], a1=geom.a1[el])
+        self._geom = geom
+
+    @property
+    def geom(self) -> ElementGeometry:
+        """Host element geometry (reference mesh.py:259-282), built on first use."""
+        if self._geom is None:
+            self._host_geometry()
+        return self._geom
+
+    @property
+    def edge_geom(self):
+        if self._edge_geom is None:
+            self._host_geometry()
+        return self._edge_geom
+
     @property
     def tensors(self):
         """Reference-form tensors (exact; lazily built, not used by the kernels)."""
@@ -311,9 +354,16 @@ class Discretization(HostSetup):
 
     def __init__(self, mesh: Mesh, scenario: Scenario, order: int, backend: str = "einsum",
                  device: int | None = None, elements=None, n_own: int | None = None,
-                 device_setup: bool | None = None, slot_order: str = "locality", halo_code=None):
-        super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup, slot_order,
-                         halo_code)
+                 device_setup: bool | None = None, slot_order: str = "locality", halo_code=None,
+                 device_tables: bool | None = None):
+        if device is not None:  # device tables and projections on that device
+            import torch
+            with torch.cuda.device(device):
+                super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup,
+                                 slot_order, halo_code, device_tables)
+        else:
+            super().__init__(mesh, scenario, order, backend, elements, n_own, device_setup,
+                             slot_order, halo_code, device_tables)
         self._setup_device(device)
 
     def _setup_device(self, device):
@@ -332,17 +382,22 @@ class Discretization(HostSetup):
         E, ld = tb.n_elem, tb.ld
         self.ld = ld
         dev = self.device
-        self._geo = torch.from_numpy(tb.geo).to(dev)
+        on = (lambda a: a.to(dev)) if self.device_tables else \
+            (lambda a: torch.from_numpy(a).to(dev))  # noqa: E731
+        self._geo = on(tb.geo)
         if self.device_setup:
             self._hb = torch.zeros((self._nh, ld), dtype=torch.float64, device=dev)
         else:
             self._hb = torch.from_numpy(self.hb_table()).to(dev)
-        self._nbr = torch.from_numpy(tb.nbr).to(dev)
-        nb = len(tb.bnd_elem)
-        self._perm = None if self.perm is None else \
-            torch.from_numpy(self.perm.astype(np.int32)).to(dev)
-        self._bel = torch.from_numpy(tb.bnd_elem).to(dev)
-        self._bloc = torch.from_numpy(tb.bnd_local).to(dev)
+        self._nbr = on(tb.nbr)
+        nb = int(tb.bnd_elem.shape[0])
+        if self.device_tables:
+            self._perm = tb.perm.to(torch.int32)
+        else:
+            self._perm = None if self.perm is None else \
+                torch.from_numpy(self.perm.astype(np.int32)).to(dev)
+        self._bel = on(tb.bnd_elem)
+        self._bloc = on(tb.bnd_local)
         self._ghost = torch.zeros(3 * max(nb, 1) * (5 * (self.k + 2) + 6), dtype=torch.float64,
                                   device=dev)
         scn = self.scn
@@ -365,7 +420,7 @@ class Discretization(HostSetup):
             (1 if (scn.forcing is not None or scn.mass_source is not None) else 0)
         # element-local Taylor sin/cos for the MMS phases: 1 = degree 9/8
         # (|z| <= 0.06), 2 = degree 7/6 (|z| <= 0.02); truncation < 1e-18
-        ang = self._max_quad_angle()
+        ang = self._max_quad_angle() if scn.device.kind == KIND_MMS else 1.0
         d.taylor = 2 if ang <= 0.02 else (1 if ang <= 0.06 else 0)
         uni = self._uniform_phase_table() if d.has_forcing else None
         self._uni = None if uni is None else torch.from_numpy(uni).to(dev)
@@ -411,7 +466,7 @@ class Discretization(HostSetup):
         if self.k > 2 or self.scn.device.kind != KIND_MMS:
             return None
         n = self.tables.n_elem
-        geo = self.tables.geo[:4, :n]
+        geo = self.tables.host("geo")[:4, :n] if self.device_tables else self.tables.geo[:4, :n]
         if n == 0:
             return None
         cls = np.unique(geo.T, axis=0)

@@ -235,3 +235,44 @@ def test_family_scenario_edited_after_construction_is_rejected():
         Discretization(mesh, bad, 1)
     with pytest.raises(ValueError):
         Discretization(mesh, dataclasses.replace(scn, g=1.0), 1)
+
+
+@pytest.mark.parametrize("case", ["unit_walls", "jitter_mms", "square_travel", "ragged"])
+def test_device_tables_equal_host_tables(case):
+    """Device-side setup (device_setup.py: connectivity by a device sort,
+    geometry, Z-order slots, SoA tables) reproduces the host NumPy setup
+    (mesh.build_connectivity / compute_geometry / locality_order /
+    layout.build_tables) bit for bit."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.device_setup import device_tables
+    from paper_1904_08684_b200.solver import HostSetup
+    mesh, scn = {
+        "unit_walls": (M.build_unit_square_mesh(48), S.bump_scenario(seed=0, cfl=0.1)),
+        "jitter_mms": (M.build_unit_square_mesh(40, jitter=0.2, seed=7), S.mms_scenario(dt=1e-4)),
+        "square_travel": (M.build_square_mesh(5, 0.2, 42), S.perturbed_square_scenario(dt=0.5)),
+        "ragged": (M.build_unit_square_mesh(13), S.mms_scenario(dt=1e-4)),
+    }[case]
+    host = HostSetup(mesh, scn, 2, device_tables=False).tables
+    dev = device_tables(mesh, scn.dirichlet_markers, scn.wall_markers, "cuda")
+    perm = HostSetup(mesh, scn, 2, device_tables=False).perm
+    assert np.array_equal(dev.host("perm"), perm)
+    assert np.array_equal(dev.host("geo"), host.geo)
+    assert np.array_equal(dev.host("nbr"), host.nbr)
+    assert np.array_equal(dev.host("bnd_elem"), host.bnd_elem)
+    assert np.array_equal(dev.host("bnd_local"), host.bnd_local)
+    assert dev.h_min == host.h_min and dev.ld == host.ld and dev.n_elem == host.n_elem
+
+
+def test_device_tables_run_matches_host_setup():
+    """A whole run on device-built tables equals the host-built one exactly."""
+    from paper_1904_08684_b200 import mesh as M, scenario as S
+    from paper_1904_08684_b200.solver import Discretization
+    mesh = M.build_unit_square_mesh(32, jitter=0.2, seed=7)
+    scn = S.bump_scenario(seed=0, cfl=0.1)
+    a = Discretization(mesh, scn, 3, device_setup=True, device_tables=False)
+    b = Discretization(mesh, scn, 3, device_setup=True, device_tables=True)
+    assert b.device_tables and not a.device_tables
+    ra = a.run(a.project_initial(), t_end=5 * a.dt)
+    rb = b.run(b.project_initial(), t_end=5 * b.dt)
+    assert a.dt == b.dt
+    assert np.array_equal(ra.c, rb.c) and np.array_equal(ra.u, rb.u)
