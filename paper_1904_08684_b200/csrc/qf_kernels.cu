@@ -550,7 +550,7 @@ struct VGroups {
 #endif
 // orders >= QF_VSPLIT solve the velocity of the new state in its own launch
 #ifndef QF_VSPLIT
-#define QF_VSPLIT 3
+#define QF_VSPLIT 4
 #endif
 template <int k>
 struct Occ {
@@ -698,12 +698,34 @@ __device__ __forceinline__ void forcing_quad(const Phys& P, const Tab& T, int e,
 // ---------------------------------------------------------- stage kernel
 // dynamic shared memory: per-order table | trace exchange (3*6*NT*BS) | BS
 // hc: out-of-block request slots per block (runtime, qf_create measures the mesh)
+// orders (bit mask) whose stage kernel stages the element's own 3K state
+// rows in shared memory with one burst of cp.async (no registers held; the
+// phases read them from there instead of re-reading global memory)
+#ifndef QF_CSMEM
+#define QF_CSMEM 8
+#endif
+// orders (bit mask) whose stage kernel evaluates the volume terms itself
+// (no volume_kernel launch, no vol[3K][ld] round trip through HBM)
+#ifndef QF_FUSEVOL
+#define QF_FUSEVOL 8
+#endif
+template <int k>
+struct FuseVol {
+  static constexpr bool value = ((QF_FUSEVOL >> k) & 1) && k >= 3;
+};
+
+template <int k>
+struct CSmem {
+  static constexpr bool value = ((QF_CSMEM >> k) & 1) && k > QF_PRE_MAXK;
+};
+
 template <int k>
 size_t stage_smem_bytes(int hc) {
   constexpr int K = Ord<k>::K, NT = Ord<k>::NT;
   constexpr int NF = FS<k>::value;
   constexpr int NU = k <= 2 ? uni_size(Ord<k>::NQ) : 0;  // MMS phase-offset table
-  return sizeof(double) * (3 * NF * NT * Blk<k>::value + NF * NT * hc + 3 * K * NT + NU) +
+  constexpr int CS = CSmem<k>::value ? 3 * K * Blk<k>::value : 0;  // own state rows
+  return sizeof(double) * (3 * NF * NT * Blk<k>::value + NF * NT * hc + 3 * K * NT + NU + CS) +
          sizeof(int) * (hc + 8);
 }
 
@@ -723,7 +745,9 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double* s_L = s_ht + NF * NT * HC;       // Lambda [3][K][NT] (neighbour edge varies by lane)
   constexpr int NU = k <= 2 ? uni_size(NQ) : 0;
   double* s_U = s_L + 3 * K * NT;          // MMS phase-offset table (Tab::uni), k <= 2
-  int* s_req = reinterpret_cast<int*>(s_U + NU);  // [HC] neighbour codes, then count
+  constexpr bool CSM = CSmem<k>::value;
+  double* s_c = s_U + NU;                  // own state rows [3K][BS] (CSM)
+  int* s_req = reinterpret_cast<int*>(s_c + (CSM ? 3 * K * BS : 0));  // [HC] neighbour codes, then count
   const double* s_tab = TB::ptr();  // per-order constants (constant memory, uniform reads)
   const int slot = threadIdx.x;
   const int blo = A.e0 + blockIdx.x * BS;
@@ -754,6 +778,12 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       for (int i = 0; i < K; ++i) own_f[5 * K + i] = i < NH ? ldg(T.hb + i * ld + ee) : 0.0;
     }
   }
+  if constexpr (CSM) {  // waited for by each thread before its first read (own rows only)
+#pragma unroll 1
+    for (int i = 0; i < 3 * K; ++i) cp_async8(s_c + i * BS + slot, A.c + i * ld + ee);
+  }
+  // own state row i: staged copy or (re-)read through L1
+  auto cown = [&](int i) { return CSM ? s_c[i * BS + slot] : ldv(A.c + i * ld + e); };
   const double t = A.t_dev ? A.t_dev[0] + A.toff * A.t_dev[1] : A.t;
   const double dt = A.t_dev ? A.t_dev[1] : A.dt;
   const double det = det2(B11, B12, B21, B22), isd = rsqrt_fast(det), sd = det * isd, idet = isd * isd;
@@ -861,9 +891,15 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
       if constexpr (PRE) {
         f = own_f + fi * K;
       } else {
-        const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+        if (CSM && fi == 0) cp_async_wait_all();
+        if (CSM && fi < 3) {
 #pragma unroll
-        for (int i = 0; i < K; ++i) fl[i] = ldv(src + i * ld + e);
+          for (int i = 0; i < K; ++i) fl[i] = s_c[(fi * K + i) * BS + slot];
+        } else {
+          const double* src = fi < 3 ? A.c + (int64_t)fi * K * ld : A.u + (int64_t)(fi - 3) * K * ld;
+#pragma unroll
+          for (int i = 0; i < K; ++i) fl[i] = ldv(src + i * ld + e);
+        }
         f = fl;
       }
       O::trace0(f, t3);
@@ -897,6 +933,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if constexpr (k <= 2 && !(V & V_TAY7)) {
     if (su) cp_async_wait_all();  // MMS phase-offset table
   }
+  if constexpr (CSM) cp_async_wait_all();  // (phase A may not have run: rhs without edges)
   __syncthreads();
   if (!active) return;
 
@@ -908,7 +945,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   double c[3 * K], u[k <= 2 ? 2 * K : 1], hb[K];
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i)
-    c[i] = (PRE && edges) ? own_f[PRE ? i : 0] : ldv(A.c + i * ld + e);
+    c[i] = (PRE && edges) ? own_f[PRE ? i : 0] : cown(i);
   if constexpr (k <= 2) {
 #pragma unroll
     for (int i = 0; i < 2 * K; ++i)
@@ -924,10 +961,16 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   if constexpr (k <= 2) {
     if (QF_EN_VOL && ((V & V_STG) || (A.terms & TERM_VOL)))
       volume_terms<k, V>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, u, hb, r);
+  } else if constexpr (FuseVol<k>::value) {  // k >= 3 volume terms in this kernel
+    if ((V & V_STG) || (A.terms & TERM_VOL)) {
+      double uu[2 * K];
+#pragma unroll
+      for (int i = 0; i < 2 * K; ++i) uu[i] = ldv(A.u + i * ld + e);
+      volume_terms<k, V>(P, B11, B12, B21, B22, isd, idet, xi, cU, cV, uu, hb, r);
+    }
   } else if (A.vol) {  // k >= 3: computed by volume_kernel (register pressure)
 #pragma unroll
     for (int i = 0; i < 3 * K; ++i) r[i] += ldg(A.vol + i * ld + e);
-
   }
   if (QF_EN_SRC && ((V & V_STG) || (A.terms & TERM_SRC))) {  // solver.py:708-725 (+ xi mass source)
     double d1, d2;
@@ -976,7 +1019,7 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
   bool fin = true;
 #pragma unroll
   for (int i = 0; i < 3 * K; ++i) {
-    double v = ldv(A.c + i * ld + e) + dt * r[i];
+    double v = cown(i) + dt * r[i];
     v = A.a != 0.0 ? fma(A.a, ldg(A.c0 + i * ld + e), A.b * v) : A.b * v;
     c[i] = v;
     fin = fin && isfinite(v);
@@ -1844,7 +1887,7 @@ static void launch_stage(qf_ctx* x, const StageArgs& a_in, cudaStream_t s) {
     g_launches++;
     a.frc = x->frc;
   }
-  if constexpr (k >= 3) {
+  if constexpr (k >= 3 && !FuseVol<k>::value) {
     if ((a.terms & TERM_VOL) && a.n > 0) {
       // one launch per input group (separate register allocation per group)
       const int vg = (a.n + 127) / 128;
@@ -2300,7 +2343,8 @@ int qf_step(qf_ctx* x, double* c, double* u, double* work, double* t_dev, void* 
 
 static int kernels_per_step(qf_ctx* x) {
   const int stages = x->d.order == 0 ? 1 : (x->d.order == 1 ? 2 : 3);
-  const int vol = x->d.order == 4 ? VGroups<4>::value : (x->d.order == 3 ? VGroups<3>::value : 0);
+  const int vol = x->d.order == 4 ? (FuseVol<4>::value ? 0 : VGroups<4>::value)
+                                  : (x->d.order == 3 ? (FuseVol<3>::value ? 0 : VGroups<3>::value) : 0);
   return stages * (1 + vol + (x->d.order >= QF_VSPLIT)) + (x->d.n_bnd > 0 ? 1 : 0) + 1;
 }
 
