@@ -114,6 +114,11 @@ int qf_project(qf_ctx* ctx, const double* prog, int32_t n, double h_min, double*
 /* Dirichlet ghost data at time t into stage table 0 (solver.py:395-402, 636-653);
  * qf_stage reads table 0, qf_step/qf_run fill all stage tables themselves. */
 int qf_ghost(qf_ctx* ctx, double t, void* stream);
+/* The same at the device time t_dev[0] + toff * t_dev[1] (t_dev = {t, dt}),
+ * and the time advance t_dev[0] += t_dev[1]: what a partitioned step needs
+ * to be replayable as a captured graph (qf_graph_*). */
+int qf_ghost_dev(qf_ctx* ctx, const double* t_dev, double toff, void* stream);
+int qf_advance_time(double* t_dev, void* stream);
 
 /* Discretization.rhs / element_rhs / edge_rhs / source_rhs / compute_lambda
  * (solver.py:340-741): rhs = sum of the masked terms at time t.
@@ -173,6 +178,21 @@ int qf_halo_table(qf_ctx* ctx, const double* ht);
  * halo push (stream memory operations, no spinning kernel). */
 int qf_signal(uint32_t* flag, uint32_t value, void* stream);
 int qf_wait(const uint32_t* flag, uint32_t value, void* stream);
+
+/* One partitioned step as a replayable CUDA graph.  qf_graph_begin starts a
+ * capture on `stream`; the caller then enqueues the step exactly as it
+ * would run it -- qf_ghost_dev, qf_stage_push with t_dev, qf_wait /
+ * qf_signal (captured as memory-operation nodes), on this and on streams
+ * forked from and joined back to it with events -- and qf_graph_end
+ * instantiates the graph.  The flag values of a step grow with the stage
+ * count, so qf_graph_launch(g, delta, stream) first adds `delta` (stages
+ * completed since the capture) to the value of every captured wait / write
+ * node, then launches.  One host call per step instead of ~10 per stage. */
+typedef struct qf_graph qf_graph;
+int qf_graph_begin(void* stream);
+int qf_graph_end(void* stream, qf_graph** out);
+int qf_graph_launch(qf_graph* g, uint32_t delta, void* stream);
+void qf_graph_destroy(qf_graph* g);
 
 /* CUDA IPC of device buffers: handle (64 bytes) + offset of ptr inside its
  * allocation; import maps a peer's allocation once per process. */

@@ -23,7 +23,8 @@ EXPORTS = (
     "qf_create", "qf_destroy", "qf_velocity", "qf_static", "qf_project", "qf_ghost", "qf_rhs", "qf_stage", "qf_step",
     "qf_run", "qf_pack", "qf_unpack", "qf_gather", "qf_scatter", "qf_error", "qf_fill", "qf_l2_error", "qf_rhs_mass",
     "qf_stage_push", "qf_signal", "qf_wait", "qf_ipc_export", "qf_ipc_import", "qf_ipc_close_all",
-    "qf_launch_count", "qf_last_error", "qf_abi_version", "qf_stage_events", "qf_rhs_ex", "qf_user_scenario", "qf_halo_traces", "qf_halo_table", "qf_copy",
+    "qf_launch_count", "qf_last_error", "qf_abi_version", "qf_stage_events", "qf_rhs_ex", "qf_user_scenario", "qf_halo_traces", "qf_halo_table", "qf_copy", "qf_ghost_dev", "qf_advance_time",
+    "qf_graph_begin", "qf_graph_end", "qf_graph_launch", "qf_graph_destroy",
 )
 
 
@@ -88,6 +89,12 @@ def load(path: Path | None = None):
         "qf_abi_version": (C.c_int, []),
         "qf_stage_events": (C.c_int, [vp, C.POINTER(C.c_void_p), i32]),
         "qf_user_scenario": (C.c_int, [vp, vp, C.c_size_t, i32]),
+        "qf_ghost_dev": (C.c_int, [vp, vp, d, vp]),
+        "qf_advance_time": (C.c_int, [vp, vp]),
+        "qf_graph_begin": (C.c_int, [vp]),
+        "qf_graph_end": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+        "qf_graph_launch": (C.c_int, [vp, C.c_uint32, vp]),
+        "qf_graph_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         if os.environ.get("QF_LIB") and not hasattr(lib, name):

@@ -17,6 +17,7 @@
 // The velocity of the new state is solved in the epilogue, so the next
 // stage's neighbour gathers read (c, u) that are already consistent and the
 // reference's separate solve at the start of each stage disappears.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -2195,6 +2196,21 @@ int qf_ghost(qf_ctx* x, double t, void* stream) {
   return cuda_check("ghost_kernel");
 }
 
+int qf_ghost_dev(qf_ctx* x, const double* t_dev, double toff, void* stream) {
+  if (!x || !t_dev) return fail(QF_E_ARG, "null argument");
+  DevGuard guard(x);
+  QF_DISPATCH(x->d.order, launch_ghost, x, 0.0, t_dev, 1, make_double3(toff, 0.0, 0.0),
+              (cudaStream_t)stream);
+  return cuda_check("ghost_kernel");
+}
+
+int qf_advance_time(double* t_dev, void* stream) {
+  if (!t_dev) return fail(QF_E_ARG, "null argument");
+  advance_time<<<1, 1, 0, (cudaStream_t)stream>>>(t_dev);
+  g_launches++;
+  return cuda_check("advance_time");
+}
+
 int qf_rhs(qf_ctx* x, const double* c, const double* u, double t, int32_t terms, double* rhs,
            double* lam, void* stream) {
   return qf_rhs_mass(x, c, u, t, terms, rhs, lam, nullptr, stream);
@@ -2525,6 +2541,108 @@ int qf_wait(const uint32_t* flag, uint32_t value, void* stream) {
   if (fn(stream, (unsigned long long)(uintptr_t)flag, value, 0) != 0)
     return fail(QF_E_CUDA, "cuStreamWaitValue32 failed");
   return QF_OK;
+}
+
+// ---------------------------------------------- captured partitioned step
+// (see include/qfswe.h).  The stream memory operations are captured as
+// batch-memop nodes; their 32-bit values are re-based before every launch.
+struct qf_graph {
+  cudaGraph_t graph = nullptr;  // kept: the memop node handles belong to it
+  cudaGraphExec_t exec = nullptr;
+  struct MemOp {
+    CUgraphNode node;
+    CUDA_BATCH_MEM_OP_NODE_PARAMS params;
+    std::vector<CUstreamBatchMemOpParams> ops;  // as captured
+  };
+  std::vector<MemOp> memops;
+  uint64_t kernels = 0;  // kernel nodes (launch count per replay)
+};
+
+typedef CUresult (*qf_pfn_memop_get)(CUgraphNode, CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+typedef CUresult (*qf_pfn_memop_set)(CUgraphExec, CUgraphNode, const CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+
+int qf_graph_begin(void* stream) {
+  if (cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return cuda_check("cudaStreamBeginCapture");
+  return QF_OK;
+}
+
+int qf_graph_end(void* stream, qf_graph** out) {
+  if (!out) return fail(QF_E_ARG, "null argument");
+  static qf_pfn_memop_get get = (qf_pfn_memop_get)driver_fn("cuGraphBatchMemOpNodeGetParams");
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture((cudaStream_t)stream, &g) != cudaSuccess || !g)
+    return cuda_check("cudaStreamEndCapture");
+  qf_graph* q = new qf_graph();
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+  // (driver-level node types: the runtime's enumeration has no batch-memop type)
+  typedef CUresult (*pfn_type)(CUgraphNode, CUgraphNodeType*);
+  static pfn_type node_type = (pfn_type)driver_fn("cuGraphNodeGetType");
+  for (cudaGraphNode_t nd : nodes) {
+    CUgraphNodeType ty;
+    if (!node_type || node_type((CUgraphNode)nd, &ty) != CUDA_SUCCESS) {
+      cudaGraphDestroy(g);
+      delete q;
+      return fail(QF_E_CUDA, "cuGraphNodeGetType failed");
+    }
+    if (ty == CU_GRAPH_NODE_TYPE_KERNEL) q->kernels++;
+    if (ty != CU_GRAPH_NODE_TYPE_BATCH_MEM_OP) continue;
+    if (!get) {
+      cudaGraphDestroy(g);
+      delete q;
+      return fail(QF_E_CUDA, "cuGraphBatchMemOpNodeGetParams unavailable");
+    }
+    qf_graph::MemOp m;
+    m.node = (CUgraphNode)nd;
+    if (get(m.node, &m.params) != CUDA_SUCCESS) {
+      cudaGraphDestroy(g);
+      delete q;
+      return fail(QF_E_CUDA, "cuGraphBatchMemOpNodeGetParams failed");
+    }
+    m.ops.assign(m.params.paramArray, m.params.paramArray + m.params.count);
+    q->memops.push_back(std::move(m));
+  }
+  cudaError_t e = cudaGraphInstantiate(&q->exec, g, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    delete q;
+    return fail(QF_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  }
+  q->graph = g;
+  *out = q;
+  return QF_OK;
+}
+
+int qf_graph_launch(qf_graph* q, uint32_t delta, void* stream) {
+  if (!q || !q->exec) return fail(QF_E_ARG, "null graph");
+  static qf_pfn_memop_set set = (qf_pfn_memop_set)driver_fn("cuGraphExecBatchMemOpNodeSetParams");
+  if (!q->memops.empty() && !set) return fail(QF_E_CUDA, "cuGraphExecBatchMemOpNodeSetParams unavailable");
+  for (auto& m : q->memops) {
+    std::vector<CUstreamBatchMemOpParams> ops = m.ops;
+    for (auto& op : ops) {
+      if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_32)
+        op.waitValue.value += delta;
+      else if (op.operation == CU_STREAM_MEM_OP_WRITE_VALUE_32)
+        op.writeValue.value += delta;
+    }
+    CUDA_BATCH_MEM_OP_NODE_PARAMS p = m.params;
+    p.paramArray = ops.data();
+    if (set((CUgraphExec)q->exec, m.node, &p) != CUDA_SUCCESS)
+      return fail(QF_E_CUDA, "cuGraphExecBatchMemOpNodeSetParams failed");
+  }
+  if (cudaGraphLaunch(q->exec, (cudaStream_t)stream) != cudaSuccess) return cuda_check("cudaGraphLaunch");
+  g_launches += q->kernels;
+  return QF_OK;
+}
+
+void qf_graph_destroy(qf_graph* q) {
+  if (!q) return;
+  if (q->exec) cudaGraphExecDestroy(q->exec);
+  if (q->graph) cudaGraphDestroy(q->graph);
+  delete q;
 }
 
 int qf_ipc_export(const void* ptr, void* handle, uint64_t* offset) {

@@ -1,24 +1,28 @@
-"""Multi-GPU: contiguous element blocks with a face-neighbour halo per stage.
+"""Multi-GPU: contiguous element blocks with a cut-edge trace halo per stage.
 
 The grid shards naturally: each rank owns a block of elements
 (vertical strips of quad columns, or px x py rectangles on the unit-square
-meshes), stores copies of the neighbour-rank elements that share an edge
-with its own (the halo) after its owned elements, and after every RK stage
-sends the new (c, u) of its cut-adjacent elements to the ranks that hold
-them as halo.  No per-stage collective exists: lambda is per edge and dt is
-fixed; one allreduce(max) fixes a CFL dt and one allreduce(max) takes the
-step time.
+meshes).  A partition holds its owned elements only; what it needs from a
+neighbour rank is, per cut edge and stage, the 6 (k + 1) trace moments (xi,
+U, V, u, v, h_b) of the neighbour element on that edge, kept in a halo trace
+table per RK buffer.  No per-stage collective exists: lambda is per edge
+and dt is fixed; one allreduce(max) fixes a CFL dt and one allreduce(max)
+takes the step time.
 
 Overlap: owned elements are ordered interior-first; per stage the interior
 range runs on the compute stream while the previous stage's halo is still in
-flight, then the cut-adjacent range runs once the halo has arrived, and its
-result is gathered and exchanged on a communication stream while the next
-stage's interior range computes.
+flight, then the cut-adjacent range runs once the halo has arrived.  With
+the p2p transport the cut-adjacent launch itself stores the new traces into
+the peers' tables (CUDA IPC / NVLink) and the ranks order their stages with
+stream memory operations on per-peer flags; the whole step of a rank --
+launches, flag waits and writes, the two streams -- is captured once as a
+CUDA graph and replayed with re-based flag values (``qf_graph_*``).  With
+the NCCL transport ``qf_halo_traces`` computes the rows and
+``batch_isend_irecv`` moves them on a communication stream.
 
 The host logic (partitioning, halo lists, exchange) is shared by the GPU
-runner (NCCL over NVLink, ``qf_stage`` / ``qf_gather`` / ``qf_scatter``) and
-a CPU runner used by the ``gloo`` tests, whose stage executor is the
-test-only oracle (``oracle/trace_stage.py``).
+runner and a CPU runner used by the ``gloo`` tests, whose stage executor is
+the test-only oracle (``oracle/trace_stage.py``).
 """
 
 from __future__ import annotations
@@ -259,6 +263,14 @@ class PartitionRunner:
                                       h.n_own, s), "qf_velocity")
         self.dt = d.dt
         self.t = 0.0
+        self.t_dev = None  # device {t, dt}: set by use_device_time (graph-replayable steps)
+
+    def use_device_time(self):
+        """Stage and Dirichlet-data times from a device {t, dt} pair advanced on
+        the stream (as the single-domain qf_step does) instead of host
+        scalars baked into every launch: a captured step can be replayed."""
+        self.t_dev = self.torch.tensor([self.t, self.dt], dtype=self.torch.float64,
+                                       device=self.disc.device)
 
     def traces_for(self, p, b=0, out=None):
         """My halo trace rows for peer p from RK buffer b (device tensor)."""
@@ -288,7 +300,12 @@ class PartitionRunner:
         """Dirichlet data of stage ``si`` (read by both ranges of the stage)."""
         d = self.disc
         if int(d.tables.bnd_elem.shape[0]):
-            self.lib.qf_ghost(d._ctx, self.t + rk_plan(self.k)[si][4] * self.dt, stream.cuda_stream)
+            toff = rk_plan(self.k)[si][4]
+            if self.t_dev is not None:
+                d._check(self.lib.qf_ghost_dev(d._ctx, self.t_dev.data_ptr(), toff,
+                                               stream.cuda_stream), "qf_ghost_dev")
+            else:
+                self.lib.qf_ghost(d._ctx, self.t + toff * self.dt, stream.cuda_stream)
 
     def stage(self, si: int, part: str, stream, ghost: bool = True, push=None, peers=None):
         """Launch stage ``si`` on the 'interior', 'boundary' or 'all' owned range
@@ -307,9 +324,10 @@ class PartitionRunner:
         e0, n = {"interior": (0, h.n_int), "boundary": (h.n_int, h.n_own - h.n_int),
                  "all": (0, h.n_own)}[part]
         if n > 0:
+            td = None if self.t_dev is None else self.t_dev.data_ptr()
             d._check(lib.qf_stage_push(d._ctx, ci.data_ptr(), ui.data_ptr(), self.c.data_ptr(),
-                                       co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, None,
-                                       0.0, e0, n, self.ht[src].data_ptr(),
+                                       co.data_ptr(), uo.data_ptr(), a, b, ts, self.dt, td,
+                                       toff if td else 0.0, e0, n, self.ht[src].data_ptr(),
                                        None if push is None else push.data_ptr(),
                                        None if peers is None else peers.data_ptr(), s),
                      "qf_stage_push")
@@ -322,6 +340,10 @@ class PartitionRunner:
             self.c.copy_(self.bufs[1][0])
             self.u.copy_(self.bufs[1][1])
             self.ht[0].copy_(self.ht[1])
+        if self.t_dev is not None:
+            self.disc._check(self.lib.qf_advance_time(
+                self.t_dev.data_ptr(), self.torch.cuda.current_stream().cuda_stream),
+                "qf_advance_time")
         self.t += self.dt
 
 
@@ -329,12 +351,14 @@ class DistributedRunner(PartitionRunner):
     """One rank of a partitioned run (one process per GPU, NCCL P2P halos)."""
 
     def __init__(self, mesh: Mesh, scenario, order: int, part: np.ndarray, rank: int,
-                 world: int, transport: str = "nccl"):
+                 world: int, transport: str = "nccl", graph: bool = True):
         import torch
         import torch.distributed as dist
 
         super().__init__(mesh, scenario, order, part, rank)
         self.dist, self.rank, self.world = dist, rank, world
+        self.use_graph = graph  # p2p transport: replay the rank's step as one CUDA graph
+        self._graph = None
         if transport not in ("nccl", "p2p"):
             raise ValueError("transport must be 'nccl' or 'p2p'")
         if transport == "p2p" and order == 0:
@@ -452,8 +476,45 @@ class DistributedRunner(PartitionRunner):
         self.dist.barrier()
 
     def _step_p2p(self):
+        """One step over the fused transport.  With ``graph`` the enqueue
+        below is captured once (stage launches, flag waits / writes, both
+        streams) and every later step is one qf_graph_launch with the flag
+        values re-based by the stages completed since the capture."""
+        import ctypes as C
+
         torch, lib = self.torch, self.lib
-        main = torch.cuda.current_stream()
+        if not self.use_graph:
+            return self._enqueue_p2p(torch.cuda.current_stream())
+        if self._graph is None:
+            # (the legacy default stream cannot capture: the graph lives on its own stream)
+            self.gstream = torch.cuda.Stream()
+            if self.t_dev is None:
+                self.use_device_time()
+            torch.cuda.synchronize()
+            gen0, t0 = self.gen, self.t
+            h, err = C.c_void_p(), None
+            with torch.cuda.stream(self.gstream):
+                self.disc._check(lib.qf_graph_begin(self.gstream.cuda_stream), "qf_graph_begin")
+                try:
+                    self._enqueue_p2p(self.gstream)
+                except Exception as exc:  # noqa: BLE001 (the capture must still be ended)
+                    err = exc
+                st = lib.qf_graph_end(self.gstream.cuda_stream, C.byref(h))
+            self.gen, self.t = gen0, t0  # the capture enqueued nothing: run the step now
+            if err is not None or st != 0 or not h.value:
+                # (e.g. a driver that cannot capture stream memory operations)
+                self.use_graph = False
+                self.graph_note = f"step graph unavailable: {err or lib.qf_last_error().decode()}"
+                return self._enqueue_p2p(torch.cuda.current_stream())
+            self._graph, self._graph_gen0 = h, gen0
+        self.gstream.wait_stream(torch.cuda.current_stream())
+        self.disc._check(lib.qf_graph_launch(self._graph, self.gen - self._graph_gen0,
+                                             self.gstream.cuda_stream), "qf_graph_launch")
+        self.gen += len(rk_plan(self.k))
+        self.t += self.dt
+
+    def _enqueue_p2p(self, main):
+        torch, lib = self.torch, self.lib
         for si in range(len(rk_plan(self.k))):
             self.ghost(si, main)
             ready = main.record_event()
@@ -506,6 +567,8 @@ class DistributedRunner(PartitionRunner):
         if self.transport == "nccl":
             main.wait_stream(self.comm)
         main.wait_stream(self.bnd)
+        if getattr(self, "gstream", None) is not None:
+            main.wait_stream(self.gstream)
 
 
 class LocalMultiRunner:

@@ -365,21 +365,27 @@ def test_l2_error_device_rejects_no_exact():
         disc.l2_error_sq(st, 0.0)
 
 
-@pytest.mark.parametrize("k", [2, 4])
-def test_p2p_transport_two_processes(k):
-    """Multi-process fused halo transport (CUDA IPC of the stage buffers,
+@pytest.mark.parametrize("k,graph,blocks,mms", [(2, 1, 0, 0), (4, 1, 0, 0), (2, 0, 0, 0), (2, 1, 1, 1),
+                                                (3, 1, 1, 0), (1, 1, 0, 1)])
+def test_p2p_transport_two_processes(k, graph, blocks, mms):
+    """Multi-process fused halo transport (CUDA IPC of the halo trace tables,
     fused push from the stage / velocity kernel, stream-memory-operation
     flags; no kernel waits on another) with 2 ranks: bit-identical to the
-    single-domain run (tools/p2p_check.py, gloo for the host objects)."""
+    single-domain run (tools/p2p_check.py, gloo for the host objects).
+    graph = 1: every rank's step is one captured CUDA graph replayed with
+    re-based flag values (qf_graph_*); blocks: block partition; mms:
+    time-dependent boundary data and forcing from the device time."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
                         "--nproc-per-node", "2", os.path.join(root, "tools", "p2p_check.py"),
-                        str(k), "3"], capture_output=True, text=True, timeout=240, cwd=root)
+                        str(k), "5", "16", str(graph), str(blocks), str(mms)],
+                       capture_output=True, text=True, timeout=240, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "bit-identical to single domain: True" in r.stdout, r.stdout[-2000:]
+    assert ("[graph]" in r.stdout) == bool(graph), r.stdout[-2000:]
 
 
 @pytest.mark.parametrize("k", [1, 2, 3])
