@@ -732,6 +732,8 @@ def bench_distributed(args, configs, metric, hooks=None):
                            "parallelism": playout,
                            "halo_transport": run.transport,
                            "halo_transport_note": run.transport_note,
+                           "step_graph": run._graph is not None,
+                           "step_graph_note": getattr(run, "graph_note", None),
                            "l2": "flushed (256 MB write) between timed steps"},
                 "gpu_launches": int(launches),
                 "e2e": {"value": 3 * K * mesh.n_triangles * ns * n_e2e / (e2e_t * 1e-3),
