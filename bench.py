@@ -44,13 +44,13 @@ CONFIGS = {
 # launches (stage_kernel, + volume_kernel + velocity_kernel for k >= 3):
 # DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) and FP64 FLOP per
 # element (2 dfma + dmul + dadd, smsp__sass_thread_inst_executed_op_*), from
-# tools/kernel_counts.sh under ncu; summaries in profiles/r01_kernel_counts.txt
+# tools/kernel_counts.sh under ncu; summaries in profiles/r02_kernel_counts.txt
 PROFILED = {
     "c1": {"bytes_per_elem": 284.6, "flop_per_elem": 2227.2},
-    "c2": {"bytes_per_elem": 481.4, "flop_per_elem": 5225.3},
-    "c3": {"bytes_per_elem": 2328.7, "flop_per_elem": 8391.9},
-    "c4": {"bytes_per_elem": 682.0, "flop_per_elem": 3289.3},
-    "c5": {"bytes_per_elem": 4125.5, "flop_per_elem": 18373.4},
+    "c2": {"bytes_per_elem": 481.5, "flop_per_elem": 5227.3},
+    "c3": {"bytes_per_elem": 1145.6, "flop_per_elem": 8332.9},
+    "c4": {"bytes_per_elem": 682.5, "flop_per_elem": 3288.3},
+    "c5": {"bytes_per_elem": 4126.4, "flop_per_elem": 18373.4},
 }
 # FP64 FMA-pipe peak of this B200, measured by tools/micro/fp64_pipes.cu
 # (DFMA 35.3 TF/s, DMMA 37.1 TF/s, one shared pipe; profiles/r01_fp64_pipes.txt)
