@@ -53,6 +53,13 @@ namespace qf {
 #ifndef QF_EUNROLL
 #define QF_EUNROLL 1
 #endif
+// orders <= QF_EUNROLL_MAXK unroll the loop over the three edges (small
+// bodies: k = 1 walls 142 -> 123 us/step, MMS 186 -> 170 at N = 512; k = 2
+// walls N = 1024 1390 -> 1474, so k >= 2 keeps the rolled loop;
+// profiles/r02_var_occ.txt)
+#ifndef QF_EUNROLL_MAXK
+#define QF_EUNROLL_MAXK 1
+#endif
 #ifndef QF_QUNROLL
 #define QF_QUNROLL 1
 #endif
@@ -239,8 +246,13 @@ enum : int {
 // shared memory (6th trace field: own element from its P1 coefficients in
 // phase A, bit-identical to qf_static; out-of-block neighbours copied from
 // the table in phase A2), so the edge loop issues no global loads
+// (round 2, after the stage-kernel variants: k = 2 is faster with the table
+// reads -- 56 instead of 65 KB of shared memory per block, 9 fewer trace
+// evaluations in phase A: C4 5.71 -> 5.48 ms/step, C2 155.9 -> 153.3 us/step,
+// profiles/r02_var_occ.txt -- so the shared-memory h_b traces are off by default)
+// (k = 1 likewise: walls 142.1 -> 139.6 us/step at N = 512)
 #ifndef QF_HBS_MAXK
-#define QF_HBS_MAXK 2
+#define QF_HBS_MAXK 0
 #endif
 template <int k>
 struct FS {
@@ -1006,7 +1018,8 @@ __global__ void __launch_bounds__(Blk<k>::value, Occ<k>::value)
     }
   }
   if (QF_EN_EDGE && edges) {  // reference solver.py:561-706
-    QF_UNROLL(QF_EUNROLL)
+    constexpr int EUN = k <= QF_EUNROLL_MAXK ? 3 : QF_EUNROLL;
+#pragma unroll EUN
     for (int j = 0; j < 3; ++j)
       edge_term<k, Blk<k>::value, V>(T, P, A, e, j, code[j], slot, blo, bhi, s_tr, s_ht, hs[j], HC, B11, B12, B21,
                    B22, isd, r);
@@ -1769,6 +1782,7 @@ __global__ void wall_scan_kernel(const int* __restrict__ nbr, int64_t ld, int n,
   }
 }
 
+#ifndef QF_KERNELS_ONLY  // (tools/one_kernel.sh: a translation unit that instantiates single kernels)
 // ===================================================================== ABI
 using namespace qf;
 
@@ -2702,3 +2716,4 @@ int qf_fill(double* buf, size_t n, double v, void* stream) {
 }
 
 }  // extern "C"
+#endif  // QF_KERNELS_ONLY
