@@ -31,4 +31,11 @@ for k in 3 4; do
       -o /tmp/${R}_k$k -f python tools/order_timing.py 512 --orders $k --once > $O/${R}_k${k}_full.log 2>&1
   python tools/ncu_summary.py /tmp/${R}_k$k.ncu-rep > $O/${R}_k${k}_kernels_ncu.txt 2>&1
 done
+# 5. setup time of C5 strong (33.5M elements) with the device-side mesh setup
+python tools/setup_time.py 4096 4 > $O/${R}_setup_time_c5_strong.json 2> $O/${R}_setup_time.err
+# 6. the multi-GPU runner at world size 1 (p2p transport + per-rank step graph; nccl)
+for t in p2p nccl; do
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 2951$((RANDOM % 10)) \
+      bench.py --gpus 1 --dist --no-cpu --no-extra --steps 100 --warmup 5 --transport $t 2>/dev/null | tail -1 > $O/${R}_bench_dist_world1_$t.json
+done
 ls -la $O

@@ -16,8 +16,8 @@ HOT = {
     "C1/C2 stage (k<=2, MMS, uni table)": r"stage_kernel<(1|2), 1158>",
     "C3-C5 stage (walls, no overflow)": r"stage_kernel<(2|3|4), 144>",
     "C5 stage (walls, overflow path)": r"stage_kernel<4, 208>",
-    "k>=3 volume": r"volume_kernel<(3|4), [01], false>",
-    "k>=3 velocity": r"velocity_kernel<(3|4), false>",
+    "k=4 volume": r"volume_kernel<4, [01], false>",
+    "k=4 velocity": r"velocity_kernel<4, false>",
 }
 GROUPS = {
     "FP64 FMA/MUL/ADD": ("DFMA", "DMUL", "DADD"),
