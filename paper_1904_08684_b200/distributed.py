@@ -675,6 +675,20 @@ def bench_distributed(args, configs, metric, hooks=None):
     for _ in range(args.warmup):
         run.step()
     run.sync()
+    # watchdog on the first steps: a halo flag that never arrives (a peer
+    # mapping that silently does not work on some topology) must end the
+    # run with a message, not hang the node until the driver's limit
+    done = torch.cuda.Event()
+    done.record()
+    t_wait = time.perf_counter()
+    while not done.query():
+        if time.perf_counter() - t_wait > float(os.environ.get("QF_DIST_WATCHDOG_S", "180")):
+            import sys
+            print(f"rank {rank}: warm-up steps did not complete within the watchdog time "
+                  f"(transport {run.transport}, step graph {run._graph is not None}); "
+                  "try --transport nccl", file=sys.stderr, flush=True)
+            os._exit(3)
+        time.sleep(0.01)
     torch.cuda.synchronize()
     dist.barrier()
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > L2
