@@ -41,6 +41,12 @@ namespace qf {
 
 #define QF_STR(x) #x
 #define QF_UNROLL(n) _Pragma(QF_STR(unroll n))
+// orders (bit mask) whose velocity kernel spills registers to shared memory
+// instead of local memory (ptxas pragma enable_smem_spilling; only kernels
+// without dynamic shared memory may use it, so not the stage kernel)
+#ifndef QF_SMEMSPILL_VEL
+#define QF_SMEMSPILL_VEL 0
+#endif
 #ifndef QF_EN_VOL
 #define QF_EN_VOL 1
 #endif
@@ -1414,6 +1420,7 @@ __global__ void __launch_bounds__(128, k == 4 ? QF_VELOCC4 : (k == 3 ? QF_VELOCC
                     unsigned* err, const int* __restrict__ push = nullptr,
                     const qf_peer* __restrict__ peers = nullptr) {
   using O = Ord<k>;
+  if constexpr (((QF_SMEMSPILL_VEL >> k) & 1) != 0) asm volatile(".pragma \"enable_smem_spilling\";");
   constexpr int K = O::K, NH = O::NH;
   const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= e0 + n) return;
