@@ -262,6 +262,7 @@ int qf_fill(double* buf, size_t n, double v, void* stream);
 /* Number of kernel launches issued through this library (all contexts). */
 uint64_t qf_launch_count(void);
 const char* qf_last_error(void);
+/* 3: + qf_ghost_dev, qf_advance_time, qf_graph_* (round 2); 2: + qf_desc.uni */
 int qf_abi_version(void);
 
 #ifdef __cplusplus

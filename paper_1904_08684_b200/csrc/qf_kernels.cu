@@ -2068,7 +2068,7 @@ static void launch_halo_traces(qf_ctx* x, const double* c, const double* u, cons
 
 extern "C" {
 
-int qf_abi_version(void) { return 2; }
+int qf_abi_version(void) { return 3; }
 const char* qf_last_error(void) { return g_last_error.c_str(); }
 uint64_t qf_launch_count(void) { return g_launches.load(); }
 

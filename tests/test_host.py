@@ -261,7 +261,7 @@ def test_cabi_exports_every_header_symbol():
     lib = _cabi.load()
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.qf_abi_version() == 2
+    assert lib.qf_abi_version() == 3
 
 
 def test_locality_order_is_a_compact_permutation():
