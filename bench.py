@@ -47,7 +47,7 @@ CONFIGS = {
 # tools/kernel_counts.sh under ncu; summaries in profiles/r02_kernel_counts.txt
 PROFILED = {
     "c1": {"bytes_per_elem": 284.6, "flop_per_elem": 2227.2},
-    "c2": {"bytes_per_elem": 529.7, "flop_per_elem": 5179.3},
+    "c2": {"bytes_per_elem": 525.9, "flop_per_elem": 5173.3},
     "c3": {"bytes_per_elem": 1145.6, "flop_per_elem": 8332.9},
     "c4": {"bytes_per_elem": 723.3, "flop_per_elem": 3226.3},
     "c5": {"bytes_per_elem": 4126.4, "flop_per_elem": 18373.4},
