@@ -31,6 +31,11 @@ for k in 3 4; do
       -o /tmp/${R}_k$k -f python tools/order_timing.py 512 --orders $k --once > $O/${R}_k${k}_full.log 2>&1
   python tools/ncu_summary.py /tmp/${R}_k$k.ncu-rep > $O/${R}_k${k}_kernels_ncu.txt 2>&1
 done
+# 4b. full capture of the C4 stage kernel (p = 2, walls, jittered mesh, 8.4M elements: the config HBM could bind)
+ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "measure/" -k regex:stage_kernel -c 1 \
+    -o /tmp/${R}_c4_stage -f python tools/kernel_counts.py c4 > $O/${R}_c4_full.log 2>&1
+python tools/ncu_summary.py /tmp/${R}_c4_stage.ncu-rep > $O/${R}_c4_stage_kernel_ncu.txt 2>&1
+python tools/ncu_regions.py /tmp/${R}_c4_stage.ncu-rep 2 >> $O/${R}_c4_stage_kernel_ncu.txt 2>&1
 # 5. setup time of C5 strong (33.5M elements) with the device-side mesh setup
 python tools/setup_time.py 4096 4 > $O/${R}_setup_time_c5_strong.json 2> $O/${R}_setup_time.err
 # 6. the multi-GPU runner at world size 1 (p2p transport + per-rank step graph; nccl)
