@@ -295,9 +295,23 @@ def measure(cfg, steps, warmup, local, n=None, e2e=False):
                                ds.t_dev.data_ptr(), 1, sp), "qf_run")
 
     def timed_steps(nsteps, sev=None, clocks=None):
+        import gc
+
         step_ms, stage_ms = [], []
+        # the step's events and graph launch are enqueued while the flush
+        # kernels still run; no collector pause may fall into that window
+        # (a host stall there would leave the GPU idle inside the events)
+        gc.collect()
+        gc.disable()
+        try:
+            return _timed_steps(nsteps, sev, clocks, step_ms, stage_ms)
+        finally:
+            gc.enable()
+
+    def _timed_steps(nsteps, sev, clocks, step_ms, stage_ms):
         for it in range(nsteps):
             flush.fill_(float(it))  # outside the timed events
+            flush.fill_(float(it) + 0.5)  # (twice: ~100 us of queue ahead of the step)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
             step()
